@@ -1,0 +1,215 @@
+"""CPU oracle for the running max-min filter (arXiv cs/0610046).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+module.  The product package ``paper_cs_0610046_b200`` never imports it and
+shares no code with it.
+
+Thin ctypes marshalling over ``liboracle.so`` (plain C, ``oracle/oracle.c`` +
+``oracle/oracle_body.inc``).  Every arithmetic step lives in the C file and
+cites the PAPER.md passage it follows:
+
+=====================  ====================================================
+``brute_1d``           definition; Table 1 naive, PAPER.md:135
+``alg1``               Algorithm 1, PAPER.md:364-401 (readings R1-R4)
+``appendix``           appendix listing
+``w3``                 Proposition (w = 3)
+``vhgw``               van Herk-Gil-Werman, PAPER.md:108-116, 176-192 (R7)
+``brute_2d``           2-D rectangle definition, valid region (R9)
+``separable_2d``       rows then columns, PAPER.md:61-63
+``batched``            ``appendix`` on every row
+``windows_at``         brute force at a list of window starts
+=====================  ====================================================
+
+Parity pins live in ``tests/test_oracle_*.py``; none of the functions is
+"parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+
+_SUFFIX = {
+    np.dtype(np.uint8): "u8",
+    np.dtype(np.int8): "i8",
+    np.dtype(np.uint16): "u16",
+    np.dtype(np.int16): "i16",
+    np.dtype(np.uint32): "u32",
+    np.dtype(np.int32): "i32",
+    np.dtype(np.uint64): "u64",
+    np.dtype(np.int64): "i64",
+    np.dtype(np.float32): "f32",
+    np.dtype(np.float64): "f64",
+}
+DTYPES = tuple(_SUFFIX)
+
+_ERRORS = {
+    -1: "window < 1 (or not 3 for w3)",
+    -2: "window larger than input",
+    -3: "NaN in input",
+    -4: "paper invariant violated (deque capacity)",
+    -5: "allocation failure",
+    -6: "bad shape",
+}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int):
+        super().__init__(f"oracle error {code}: {_ERRORS.get(code, 'unknown')}")
+        self.code = code
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("comparisons", ctypes.c_uint64), ("peak_wedge", ctypes.c_int64)]
+
+
+@dataclass
+class Stats:
+    comparisons: int
+    peak_wedge: int
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (plain -O2, IEEE-exact: no fast-math)."""
+    src = [os.path.join(_HERE, "oracle.c"), os.path.join(_HERE, "oracle_body.inc"),
+           os.path.join(_HERE, "oracle.h")]
+    if not force and os.path.exists(_LIB_PATH):
+        if os.path.getmtime(_LIB_PATH) >= max(os.path.getmtime(s) for s in src):
+            return _LIB_PATH
+    subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-shared", "-fPIC", "-o",
+                           _LIB_PATH, src[0]])
+    return _LIB_PATH
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = ctypes.CDLL(_LIB_PATH)
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _fn(name: str, dtype):
+    dt = np.dtype(dtype)
+    if dt not in _SUFFIX:
+        raise TypeError(f"oracle: unsupported dtype {dt}")
+    f = getattr(_load(), f"oracle_{name}_{_SUFFIX[dt]}")
+    f.restype = ctypes.c_int
+    return f
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise OracleError(rc)
+
+
+def _run_1d(name: str, a, w: int):
+    a = np.ascontiguousarray(a)
+    n = a.shape[0]
+    m = max(n - w + 1, 0)
+    mx = np.empty(m, a.dtype)
+    mn = np.empty(m, a.dtype)
+    st = _Stats()
+    _check(_fn(name, a.dtype)(_ptr(a), ctypes.c_int64(n), ctypes.c_int64(w), _ptr(mx),
+                              _ptr(mn), ctypes.byref(st)))
+    return mx, mn, Stats(int(st.comparisons), int(st.peak_wedge))
+
+
+def brute_1d(a, w: int):
+    """O1, the definition.  Returns (max, min, Stats)."""
+    return _run_1d("brute_1d", a, w)
+
+
+def alg1(a, w: int):
+    """O2, Algorithm 1 read literally.  w >= 2."""
+    return _run_1d("alg1", a, w)
+
+
+def appendix(a, w: int):
+    """O3, the appendix C++ listing.  w >= 1."""
+    return _run_1d("appendix", a, w)
+
+
+def vhgw(a, w: int):
+    """van Herk-Gil-Werman baseline."""
+    return _run_1d("vhgw", a, w)
+
+
+def w3(a):
+    """Proposition w = 3."""
+    a = np.ascontiguousarray(a)
+    n = a.shape[0]
+    m = max(n - 2, 0)
+    mx = np.empty(m, a.dtype)
+    mn = np.empty(m, a.dtype)
+    st = _Stats()
+    _check(_fn("w3", a.dtype)(_ptr(a), ctypes.c_int64(n), _ptr(mx), _ptr(mn),
+                              ctypes.byref(st)))
+    return mx, mn, Stats(int(st.comparisons), int(st.peak_wedge))
+
+
+def batched(a, w: int, n: int | None = None):
+    """``appendix`` on every row of a 2-D array ``a[batch, ld]`` (first n columns)."""
+    a = np.ascontiguousarray(a)
+    batch, ld = a.shape
+    n = ld if n is None else n
+    m = n - w + 1
+    mx = np.empty((batch, max(m, 0)), a.dtype)
+    mn = np.empty((batch, max(m, 0)), a.dtype)
+    _check(_fn("batched", a.dtype)(_ptr(a), ctypes.c_int64(batch), ctypes.c_int64(n),
+                                   ctypes.c_int64(ld), ctypes.c_int64(w), _ptr(mx), _ptr(mn),
+                                   ctypes.c_int64(max(m, 1))))
+    return mx, mn
+
+
+def _run_2d(name: str, a, w_row: int, w_col: int):
+    a = np.ascontiguousarray(a)
+    squeeze = a.ndim == 2
+    if squeeze:
+        a = a[None]
+    batch, rows, cols = a.shape
+    R, C = rows - w_col + 1, cols - w_row + 1
+    mx = np.empty((batch, max(R, 0), max(C, 0)), a.dtype)
+    mn = np.empty_like(mx)
+    _check(_fn(name, a.dtype)(_ptr(a), ctypes.c_int64(batch), ctypes.c_int64(rows),
+                              ctypes.c_int64(cols), ctypes.c_int64(w_row), ctypes.c_int64(w_col),
+                              _ptr(mx), _ptr(mn)))
+    if squeeze:
+        return mx[0], mn[0]
+    return mx, mn
+
+
+def brute_2d(a, w_row: int, w_col: int):
+    """2-D rectangle max/min over the valid region (reading R9)."""
+    return _run_2d("brute_2d", a, w_row, w_col)
+
+
+def separable_2d(a, w_row: int, w_col: int):
+    """Rows first, then columns, ``appendix`` as the 1-D filter."""
+    return _run_2d("separable_2d", a, w_row, w_col)
+
+
+def windows_at(a, w: int, starts):
+    """Brute-force max/min of the windows starting at ``starts`` (spot checks)."""
+    a = np.ascontiguousarray(a)
+    starts = np.ascontiguousarray(starts, dtype=np.int64)
+    mx = np.empty(starts.shape[0], a.dtype)
+    mn = np.empty(starts.shape[0], a.dtype)
+    _check(_fn("windows_at", a.dtype)(_ptr(a), ctypes.c_int64(a.shape[0]), ctypes.c_int64(w),
+                                      _ptr(starts), ctypes.c_int64(starts.shape[0]), _ptr(mx),
+                                      _ptr(mn)))
+    return mx, mn

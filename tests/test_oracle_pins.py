@@ -1,0 +1,292 @@
+"""Pins for the CPU oracle (oracle/), independent of the oracle itself.
+
+Each pin comes from outside the function it checks: worked examples re-derived by
+hand (tests/golden, cited), an independent library implementation of the
+definition (numpy sliding_window_view + max/min), closed forms, the paper's
+invariants (Table 1), exhaustive brute force
+on tiny inputs, and metamorphic identities.  No GPU.
+"""
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+swv = np.lib.stride_tricks.sliding_window_view
+
+
+def np_filter(a, w):
+    """Independent implementation of the definition PAPER.md:39-42 (numpy)."""
+    v = swv(np.asarray(a), w)
+    return v.max(axis=1), v.min(axis=1)
+
+
+def np_filter_2d(a, w_row, w_col):
+    v = swv(np.asarray(a), (w_col, w_row), axis=(-2, -1))
+    return v.max(axis=(-2, -1)), v.min(axis=(-2, -1))
+
+
+def same(x, y):
+    x = np.asarray(x)
+    y = np.asarray(y)
+    return x.shape == y.shape and x.dtype == y.dtype and x.tobytes() == y.tobytes()
+
+
+def all_1d(a, w):
+    """Every 1-D oracle variant applicable to (a, w): name -> (max, min, stats)."""
+    out = {"brute": oracle.brute_1d(a, w), "appendix": oracle.appendix(a, w),
+           "vhgw": oracle.vhgw(a, w)}
+    if w >= 2:
+        out["alg1"] = oracle.alg1(a, w)
+    if w == 3:
+        out["w3"] = oracle.w3(a)
+    return out
+
+
+# ---------------------------------------------------------------- golden ----
+
+def test_golden_examples_1d():
+    g = json.load(open(os.path.join(GOLDEN, "examples_1d.json")))
+    for case in g["cases"]:
+        a = np.array(case["a"], np.float64)
+        for name, (mx, mn, _) in all_1d(a, case["w"]).items():
+            assert mx.tolist() == case["max"], (name, case["cite"])
+            assert mn.tolist() == case["min"], (name, case["cite"])
+
+
+def test_golden_naive_count():
+    g = json.load(open(os.path.join(GOLDEN, "examples_1d.json")))
+    for c in g["counts"]:
+        a = synth.uniform_f64(11, 0, c["n"])
+        _, _, st = oracle.brute_1d(a, c["w"])
+        assert st.comparisons == c["naive_comparisons"], c["cite"]
+
+
+def test_golden_examples_2d():
+    g = json.load(open(os.path.join(GOLDEN, "examples_2d.json")))
+    for case in g["cases"]:
+        a = np.array(case["a"], np.float64)
+        for f in (oracle.brute_2d, oracle.separable_2d):
+            mx, mn = f(a, case["w_row"], case["w_col"])
+            assert mx.tolist() == case["max"], case["cite"]
+            assert mn.tolist() == case["min"], case["cite"]
+
+
+# ------------------------------------------------- brute force / numpy -----
+
+def test_exhaustive_tiny_alphabet():
+    """All arrays of length <= 8 over {0,1,2}, every w (73 812 cases)."""
+    count = 0
+    for n in range(1, 9):
+        for tup in itertools.product((0.0, 1.0, 2.0), repeat=n):
+            a = np.array(tup)
+            for w in range(1, n + 1):
+                ex, en = np_filter(a, w)
+                for name, (mx, mn, st) in all_1d(a, w).items():
+                    assert same(mx, ex) and same(mn, en), (name, tup, w)
+                    if name in ("alg1", "appendix"):
+                        assert st.comparisons <= 3 * n, (name, tup, w)
+                        assert st.peak_wedge <= w + 1, (name, tup, w)
+                count += 1
+    assert count == 73812
+
+
+@pytest.mark.parametrize("alphabet", [None, 8])
+def test_random_cases_vs_numpy(alphabet):
+    """SPEC.md:397 recipe: 1000 cases, n in [1,256], w in [1,n], continuous and {0..7}."""
+    for k in range(1000):
+        n = 1 + synth.rng(21, 0, k) % 256
+        w = 1 + synth.rng(21, 1, k) % n
+        a = synth.random_values(np.float64, n, seed=22 + k, alphabet=alphabet)
+        ex, en = np_filter(a, w)
+        for name, (mx, mn, st) in all_1d(a, w).items():
+            assert same(mx, ex) and same(mn, en), (name, n, w, k)
+
+
+@pytest.mark.parametrize("dtype", oracle.DTYPES)
+def test_every_dtype_vs_numpy(dtype):
+    """Full-range values (incl. > 2^53 for 64-bit ints, negative floats)."""
+    for k, (n, w) in enumerate([(1, 1), (7, 3), (300, 17), (1000, 1000), (4097, 129)]):
+        a = synth.random_values(dtype, n, seed=31 + k)
+        ex, en = np_filter(a, w)
+        mx, mn, _ = oracle.appendix(a, w)
+        assert same(mx, ex) and same(mn, en), (dtype, n, w)
+        mx, mn, _ = oracle.brute_1d(a, w)
+        assert same(mx, ex) and same(mn, en), (dtype, n, w)
+    info = np.iinfo(dtype) if np.dtype(dtype).kind in "iu" else np.finfo(dtype)
+    a = np.array([info.max, info.min, 0, info.max, info.min], dtype)
+    ex, en = np_filter(a, 2)
+    mx, mn, _ = oracle.appendix(a, 2)
+    assert same(mx, ex) and same(mn, en)
+
+
+def test_windows_at_and_batched_vs_numpy():
+    a = synth.random_values(np.float32, 5000, seed=41)
+    starts = np.array([0, 1, 17, 4000, 5000 - 300], np.int64)
+    mx, mn = oracle.windows_at(a, 300, starts)
+    ex, en = np_filter(a, 300)
+    assert same(mx, ex[starts]) and same(mn, en[starts])
+    b = synth.random_values(np.float32, 7 * 200, seed=42).reshape(7, 200)
+    mx, mn = oracle.batched(b, 33)
+    for r in range(7):
+        ex, en = np_filter(b[r], 33)
+        assert same(mx[r], ex) and same(mn[r], en)
+
+
+# ------------------------------------------------------------ closed forms --
+
+def test_closed_forms():
+    n = 1000
+    up = synth.ramp_up(n)
+    down = synth.ramp_down(n)
+    for w in (1, 2, 3, 10, 999, 1000):
+        for name, (mx, mn, _) in all_1d(up, w).items():  # non-decreasing
+            assert same(mx, up[w - 1:]) and same(mn, up[: n - w + 1]), name
+        for name, (mx, mn, _) in all_1d(down, w).items():  # non-increasing
+            assert same(mx, down[: n - w + 1]) and same(mn, down[w - 1:]), name
+        c = synth.constant(n, 7.0)
+        for name, (mx, mn, _) in all_1d(c, w).items():
+            assert (mx == 7.0).all() and (mn == 7.0).all(), name
+    a = synth.uniform_f64(5, 0, n)
+    for name, (mx, mn, _) in all_1d(a, 1).items():  # w = 1: identity
+        assert same(mx, a) and same(mn, a), name
+    for name, (mx, mn, _) in all_1d(a, n).items():  # w = n: global max/min
+        assert mx.tolist() == [a.max()] and mn.tolist() == [a.min()], name
+    alt = synth.alternating(n)
+    for w in (2, 3, 50):
+        for name, (mx, mn, _) in all_1d(alt, w).items():
+            assert (mx == 1.0).all() and (mn == 0.0).all(), name
+
+
+# -------------------------------------------------------------- invariants --
+
+FAMILIES = {
+    "uniform": lambda n: synth.uniform_f64(3, 0, n),
+    "sine": lambda n: synth.sine(n, 10000),
+    "ramp_up": synth.ramp_up,
+    "ramp_down": synth.ramp_down,
+    "constant": lambda n: synth.constant(n, 7.0),
+    "alternating": synth.alternating,
+    "piecewise": lambda n: synth.piecewise(n, 40, seed=4),
+    "tie_alphabet": lambda n: synth.random_values(np.float64, n, seed=6, alphabet=8),
+}
+
+
+@pytest.mark.parametrize("family", sorted(FAMILIES))
+def test_comparison_bounds(family):
+    """Prop. PAPER.md:406-410 (<= 3n), Prop. PAPER.md:477-479 (<= 2n if monotone),
+    Prop. PAPER.md:494-497 (size(U)+size(L) <= w+1); SPEC.md:398-403 grid."""
+    n = 100_000
+    a = FAMILIES[family](n)
+    monotone = family in ("ramp_up", "ramp_down", "constant")
+    for w in (3, 10, 100, 1000, 10_000):
+        ex, en = np_filter(a, w)
+        for f in (oracle.alg1, oracle.appendix):
+            mx, mn, st = f(a, w)
+            assert same(mx, ex) and same(mn, en)
+            assert st.comparisons <= 3 * n
+            assert st.peak_wedge <= w + 1
+            if monotone:
+                assert st.comparisons <= 2 * n
+                # hand derivation: on a monotone input each loop step does the
+                # line-379 comparison and the while loop never runs
+                assert st.comparisons == n - 1
+
+
+def test_iid_cost_approaches_three():
+    """Survey measurement: i.i.d. input at w=1000 costs
+    ~2.996 comparisons per element -- close to, never above, the bound 3."""
+    n = 100_000
+    a = synth.uniform_f64(3, 0, n)
+    _, _, st = oracle.alg1(a, 1000)
+    assert 2.95 < st.comparisons / n <= 3.0
+
+
+def test_naive_count_formula():
+    """Table 1 naive row (2w-2 per element), exact."""
+    n = 1000
+    a = synth.uniform_f64(7, 0, n)
+    for w in (1, 2, 10, 100, 1000):
+        _, _, st = oracle.brute_1d(a, w)
+        assert st.comparisons == (n - w + 1) * 2 * (w - 1)
+
+
+def test_vhgw_bound():
+    """Table 1: van Herk-Gil-Werman <= 6-8/w comparisons per element on
+    block-aligned inputs."""
+    for w in (4, 16, 64):
+        n = 100 * w
+        for fam in ("uniform", "sine", "alternating", "ramp_up"):
+            a = FAMILIES[fam](n)
+            mx, mn, st = oracle.vhgw(a, w)
+            ex, en = np_filter(a, w)
+            assert same(mx, ex) and same(mn, en)
+            assert st.comparisons <= (6 - 8 / w) * n
+
+
+def test_w3_two_comparisons():
+    """Proposition: w = 3 in <= 2 comparisons per element."""
+    n = 100_000
+    for fam in sorted(FAMILIES):
+        a = FAMILIES[fam](n)
+        mx, mn, st = oracle.w3(a)
+        ex, en = np_filter(a, 3)
+        assert same(mx, ex) and same(mn, en), fam
+        assert st.comparisons <= 2 * n
+
+
+# ------------------------------------------------------------------ 2-D -----
+
+def test_2d_separable_equals_rectangles():
+    """50 seeded 64x64 grids, (w_row, w_col) in {1..8}^2."""
+    for g in range(50):
+        a = synth.random_values(np.float32, 64 * 64, seed=100 + g,
+                                alphabet=16 if g % 2 else None).reshape(64, 64)
+        pairs = [(wr, wc) for wr in range(1, 9) for wc in range(1, 9)]
+        if g >= 4:  # all 64 pairs on 4 grids, 8 seeded pairs on the rest
+            pairs = [pairs[synth.rng(101, g, k) % 64] for k in range(8)]
+        for wr, wc in pairs:
+            ex, en = np_filter_2d(a, wr, wc)
+            bx, bn = oracle.brute_2d(a, wr, wc)
+            sx, sn = oracle.separable_2d(a, wr, wc)
+            assert same(bx, ex) and same(bn, en), (g, wr, wc)
+            assert same(sx, ex) and same(sn, en), (g, wr, wc)
+
+
+def test_2d_transpose_symmetry_and_batch():
+    a = synth.c4(count=2, rows=70, cols=90, nrect=5)
+    mx, mn = oracle.separable_2d(a, 5, 9)
+    tx, tn = oracle.separable_2d(np.ascontiguousarray(a.transpose(0, 2, 1)), 9, 5)
+    assert same(mx, np.ascontiguousarray(tx.transpose(0, 2, 1)))
+    assert same(mn, np.ascontiguousarray(tn.transpose(0, 2, 1)))
+    for b in range(2):
+        ex, en = np_filter_2d(a[b], 5, 9)
+        assert same(mx[b], ex) and same(mn[b], en)
+
+
+# --------------------------------------------------------------- errors -----
+
+def test_errors():
+    a = np.arange(5, dtype=np.float64)
+    for f in (oracle.brute_1d, oracle.appendix, oracle.vhgw, oracle.alg1):
+        with pytest.raises(oracle.OracleError) as e:
+            f(a, 0)
+        assert e.value.code == -1
+        with pytest.raises(oracle.OracleError) as e:
+            f(a, 6)
+        assert e.value.code == -2
+    b = a.copy()
+    b[2] = np.nan
+    for f in (oracle.brute_1d, oracle.appendix, oracle.alg1, oracle.vhgw):
+        with pytest.raises(oracle.OracleError) as e:
+            f(b, 2)
+        assert e.value.code == -3
+    with pytest.raises(oracle.OracleError):
+        oracle.alg1(a, 1)  # reading R4: Algorithm 1 needs w >= 2
+    with pytest.raises(oracle.OracleError):
+        oracle.brute_2d(np.zeros((3, 3)), 4, 1)
