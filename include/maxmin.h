@@ -1,0 +1,163 @@
+/*
+ * maxmin.h -- C ABI of libmaxmin.so, the B200 (sm_100a) running max-min filter.
+ *
+ * The operation (arXiv cs/0610046 section 1):
+ *   given a_0..a_{n-1} and a window width w, for every j in [0, n-w]
+ *     out_max[j] = max_{i in [j, j+w)} a_i      out_min[j] = min_{i in [j, j+w)} a_i
+ *   -- "the maximum and the minimum over all windows of size w".  There are
+ *   m = n-w+1 windows.  Both filters are produced in one pass that reads the
+ *   input once (the running max and min filters alone, are the
+ *   same calls with one output pointer NULL).
+ * 2-D: "applying the unidimensional [filter] on rows and then
+ *   on columns"; only the valid region is produced (reading R9).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ * - All data pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors)
+ *   owned by the caller, except the *_host entry points whose data pointers
+ *   are HOST pointers.  The library never allocates or frees caller memory;
+ *   scratch space is passed in through `workspace`.
+ * - Lengths, counts, leading dimensions and strides are in ELEMENTS (int64).
+ * - Work is enqueued asynchronously on `stream` (a cudaStream_t passed as
+ *   void*; NULL = legacy default stream) of the current device.  Argument
+ *   errors are detected synchronously: nothing is launched and a non-zero
+ *   status is returned.  A launch failure returns MAXMIN_ERR_CUDA and
+ *   maxmin_last_cuda_error() reports the cudaError_t.
+ * - Alignment: data pointers must be 16-byte aligned and every leading
+ *   dimension / stride times sizeof(element) must be a multiple of 16 bytes
+ *   (else MAXMIN_ERR_ALIGNMENT).  Loads never touch bytes outside the 16-byte
+ *   granules that contain input elements.
+ * - Outputs must not overlap the input or each other (MAXMIN_ERR_ALIAS).
+ * - Preconditions not checked: floating-point inputs contain no NaN; -0.0 and
+ *   +0.0 compare equal and either may be returned.  Every output element is a
+ *   copy of an input element, so under these preconditions results are
+ *   bit-identical to any correct implementation (the CPU oracle).
+ * - Thread safety: stateless; concurrent calls on different streams are safe
+ *   provided they use distinct workspaces.
+ */
+#ifndef MAXMIN_H
+#define MAXMIN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MAXMIN_U8 = 0,
+  MAXMIN_I8 = 1,
+  MAXMIN_U16 = 2,
+  MAXMIN_I16 = 3,
+  MAXMIN_U32 = 4,
+  MAXMIN_I32 = 5,
+  MAXMIN_U64 = 6,
+  MAXMIN_I64 = 7,
+  MAXMIN_F32 = 8,
+  MAXMIN_F64 = 9
+} maxmin_dtype;
+
+typedef enum {
+  MAXMIN_OK = 0,
+  MAXMIN_ERR_NULL = 1,              /* a required pointer is NULL, or both outputs NULL */
+  MAXMIN_ERR_DTYPE = 2,             /* unknown dtype (2-D: see maxmin_filter_2d)       */
+  MAXMIN_ERR_WINDOW = 3,            /* w < 1                                           */
+  MAXMIN_ERR_WINDOW_TOO_LARGE = 4,  /* w > n (2-D: w_row > cols or w_col > rows)       */
+  MAXMIN_ERR_SHAPE = 5,             /* n < 1, batch < 0, ld too small, size overflow   */
+  MAXMIN_ERR_ALIGNMENT = 6,         /* pointer / leading dimension not 16-byte aligned  */
+  MAXMIN_ERR_ALIAS = 7,             /* an output overlaps the input or the other output */
+  MAXMIN_ERR_WORKSPACE = 8,         /* workspace NULL or smaller than required          */
+  MAXMIN_ERR_CUDA = 9,              /* a CUDA runtime call failed                       */
+  MAXMIN_ERR_UNSUPPORTED = 10,      /* valid request outside this build's limits        */
+  MAXMIN_ERR_MEMORY = 11            /* a data pointer is not device memory (device APIs) */
+} maxmin_status;
+
+/* Human-readable name of a status code (static storage). */
+const char *maxmin_status_str(int status);
+
+/* cudaError_t of the last failing CUDA call made by this library in the
+   calling thread (0 if none). */
+int maxmin_last_cuda_error(void);
+
+/* Library version, e.g. "maxmin-b200 0.1 sm_100a". */
+const char *maxmin_version(void);
+
+/* Size in bytes of one element of dtype `dt`, or 0 if unknown. */
+size_t maxmin_dtype_size(int dt);
+
+/*
+ * Workspace needed by maxmin_filter_1d / maxmin_filter_batched for these
+ * arguments, written to *bytes.  It is 0 unless the window exceeds the on-chip
+ * halo (the cross-CTA look-back path, DESIGN.md kernel "large"), where it is
+ * ~ (batch * (n + w) / tile) * (4 + 2 * 2 * sizeof(T)) + 256 bytes.
+ */
+int maxmin_workspace_bytes(int dt, int64_t batch, int64_t n, int64_t w,
+                           size_t *bytes);
+
+/*
+ * 1-D running max-min filter.
+ *   in        device, n elements of dtype dt (contiguous).
+ *   n, w      1 <= w <= n.
+ *   out_max   device, n-w+1 elements, or NULL to skip the max filter.
+ *   out_min   device, n-w+1 elements, or NULL to skip the min filter.
+ *   workspace device scratch of maxmin_workspace_bytes(dt,1,n,w) bytes (may be
+ *             NULL when that is 0).  Must not be used concurrently by another
+ *             call.  Contents on entry are ignored.
+ */
+int maxmin_filter_1d(int dt, const void *in, int64_t n, int64_t w,
+                     void *out_max, void *out_min, void *workspace,
+                     size_t workspace_bytes, void *stream);
+
+/*
+ * Batched series: the 1-D filter on each of `batch` independent rows (no halo
+ * between rows).  Row b is in + b*in_ld (n elements, in_ld >= n); its outputs
+ * are out_* + b*out_ld (n-w+1 elements, out_ld >= n-w+1).  batch == 0 is a
+ * no-op.  Workspace as maxmin_workspace_bytes(dt, batch, n, w).
+ */
+int maxmin_filter_batched(int dt, const void *in, int64_t batch, int64_t n,
+                          int64_t in_ld, int64_t w, void *out_max,
+                          void *out_min, int64_t out_ld, void *workspace,
+                          size_t workspace_bytes, void *stream);
+
+/*
+ * 2-D separable max-min filter over `batch` images.
+ *   Image b, row r, column c is in[b*in_bstride + r*in_ld + c].
+ *   w_row is the window along a row (over columns, 1 <= w_row <= cols),
+ *   w_col the window down a column (over rows, 1 <= w_col <= rows).
+ *   Output (b, r, c), r in [0, rows-w_col], c in [0, cols-w_row], is the max
+ *   (min) over rows [r, r+w_col) x columns [c, c+w_row), stored at
+ *   out_*[b*out_bstride + r*out_ld + c].  Only the valid region is written.
+ *   Requires in_ld >= cols, out_ld >= cols-w_row+1, in_bstride >= rows*in_ld,
+ *   out_bstride >= (rows-w_col+1)*out_ld (or batch == 1).
+ *   Unlike the 1-D calls, pointers and strides need only element alignment.
+ *   Supported dtypes: all.  The fused single-pass kernel keeps the
+ *   (32+w_col-1) x (256/sizeof(T)+w_row-1) input box on chip; requests whose
+ *   box exceeds 200 KB of shared memory return MAXMIN_ERR_UNSUPPORTED.
+ */
+int maxmin_filter_2d(int dt, const void *in, int64_t batch, int64_t rows,
+                     int64_t cols, int64_t in_ld, int64_t in_bstride,
+                     int64_t w_row, int64_t w_col, void *out_max,
+                     void *out_min, int64_t out_ld, int64_t out_bstride,
+                     void *stream);
+
+/*
+ * End-to-end 1-D call on HOST buffers (in, out_max, out_min are host
+ * pointers; page-locked memory gives full PCIe bandwidth).  The input is
+ * streamed to the device in chunks (with a (w-1)-element overlap), filtered
+ * and streamed back, with copies and kernels of consecutive chunks
+ * overlapped on two streams.  `dev_workspace` is device scratch of
+ * maxmin_host_workspace_bytes(dt, n, w, chunk) bytes.  `chunk` is the number
+ * of windows per chunk (0 = default 2^24).  Returns after the results are in
+ * the host buffers (synchronous).
+ */
+int maxmin_host_workspace_bytes(int dt, int64_t n, int64_t w, int64_t chunk,
+                                size_t *bytes);
+int maxmin_filter_1d_host(int dt, const void *in, int64_t n, int64_t w,
+                          void *out_max, void *out_min, int64_t chunk,
+                          void *dev_workspace, size_t workspace_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MAXMIN_H */

@@ -1,0 +1,155 @@
+"""B200-native running max-min filter (arXiv cs/0610046).
+
+Python binding of libmaxmin.so with the names of the C ABI (include/maxmin.h).
+Marshalling only: tensors are PyTorch CUDA tensors (device memory + the current
+stream); every step of the filter runs in the library's sm_100a kernels.  There
+is no CPU fallback -- a missing library raises.
+
+    out_max[j] = max a[j .. j+w)   out_min[j] = min a[j .. j+w)
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import MaxMinError
+
+__all__ = [
+    "MaxMinError", "dtype_code", "maxmin_workspace_bytes", "maxmin_filter_1d",
+    "maxmin_filter_batched", "maxmin_filter_2d", "maxmin_filter_1d_host",
+    "maxmin_host_workspace_bytes", "version",
+]
+
+_CODES = {
+    torch.uint8: _lib.U8, torch.int8: _lib.I8, torch.uint16: _lib.U16, torch.int16: _lib.I16,
+    torch.uint32: _lib.U32, torch.int32: _lib.I32, torch.uint64: _lib.U64, torch.int64: _lib.I64,
+    torch.float32: _lib.F32, torch.float64: _lib.F64,
+}
+
+
+def dtype_code(dtype) -> int:
+    try:
+        return _CODES[dtype]
+    except KeyError:
+        raise TypeError(f"maxmin: unsupported dtype {dtype}") from None
+
+
+def version() -> str:
+    return _lib.lib().maxmin_version().decode()
+
+
+def _stream_ptr(stream) -> ctypes.c_void_p:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def maxmin_workspace_bytes(dtype, batch: int, n: int, w: int) -> int:
+    out = ctypes.c_size_t(0)
+    _lib.check(_lib.lib().maxmin_workspace_bytes(dtype_code(dtype), batch, n, w, ctypes.byref(out)))
+    return int(out.value)
+
+
+def _workspace(dtype, batch, n, w, device, workspace):
+    need = maxmin_workspace_bytes(dtype, batch, n, w)
+    if need == 0:
+        return None, 0
+    if workspace is None:
+        workspace = torch.empty(need, dtype=torch.uint8, device=device)
+    return workspace, workspace.numel() * workspace.element_size()
+
+
+def maxmin_filter_1d(x: torch.Tensor, w: int, out_max=None, out_min=None, *, want_max=True,
+                     want_min=True, workspace=None, stream=None):
+    """Running max and min of a contiguous 1-D CUDA tensor; returns (out_max, out_min)."""
+    if x.dim() != 1 or not x.is_cuda or not x.is_contiguous():
+        raise ValueError("maxmin_filter_1d: x must be a contiguous 1-D CUDA tensor")
+    n = x.shape[0]
+    m = max(n - w + 1, 0)
+    if want_max and out_max is None and m > 0:
+        out_max = torch.empty(m, dtype=x.dtype, device=x.device)
+    if want_min and out_min is None and m > 0:
+        out_min = torch.empty(m, dtype=x.dtype, device=x.device)
+    ws, wsb = _workspace(x.dtype, 1, n, w, x.device, workspace) if 1 <= w <= n else (None, 0)
+    _lib.check(_lib.lib().maxmin_filter_1d(dtype_code(x.dtype), _ptr(x), n, w, _ptr(out_max),
+                                           _ptr(out_min), _ptr(ws), wsb, _stream_ptr(stream)))
+    return out_max, out_min
+
+
+def maxmin_filter_batched(x: torch.Tensor, w: int, n: int | None = None, out_max=None, out_min=None,
+                          *, want_max=True, want_min=True, workspace=None, stream=None):
+    """The 1-D filter on every row of a 2-D CUDA tensor [batch, ld] (first n columns)."""
+    if x.dim() != 2 or not x.is_cuda or x.stride(1) != 1:
+        raise ValueError("maxmin_filter_batched: x must be a row-major 2-D CUDA tensor")
+    batch, ncols = x.shape
+    n = ncols if n is None else n
+    m = max(n - w + 1, 0)
+    # rows of the outputs are padded to 16 bytes (the C ABI's alignment rule)
+    vec = max(16 // x.element_size(), 1)
+    m_pad = (m + vec - 1) // vec * vec
+    if want_max and out_max is None and m > 0:
+        out_max = torch.empty(batch, m_pad, dtype=x.dtype, device=x.device)[:, :m]
+    if want_min and out_min is None and m > 0:
+        out_min = torch.empty(batch, m_pad, dtype=x.dtype, device=x.device)[:, :m]
+    out_ld = (out_max if out_max is not None else out_min).stride(0) if m > 0 else 1
+    ws, wsb = _workspace(x.dtype, batch, n, w, x.device, workspace) if 1 <= w <= n else (None, 0)
+    _lib.check(_lib.lib().maxmin_filter_batched(dtype_code(x.dtype), _ptr(x), batch, n, x.stride(0), w,
+                                                _ptr(out_max), _ptr(out_min), out_ld, _ptr(ws), wsb,
+                                                _stream_ptr(stream)))
+    return out_max, out_min
+
+
+def maxmin_filter_2d(x: torch.Tensor, w_row: int, w_col: int, cols: int | None = None, out_max=None,
+                     out_min=None, *, want_max=True, want_min=True, stream=None):
+    """Separable 2-D max/min over a [batch, rows, ld] (or [rows, ld]) CUDA tensor.
+
+    Output (b, r, c) covers rows [r, r+w_col) x columns [c, c+w_row); only the valid
+    region (rows-w_col+1) x (cols-w_row+1) is computed.
+    """
+    squeeze = x.dim() == 2
+    xx = x[None] if squeeze else x
+    if xx.dim() != 3 or not xx.is_cuda or xx.stride(2) != 1:
+        raise ValueError("maxmin_filter_2d: x must be a row-major [batch, rows, ld] CUDA tensor")
+    batch, rows, ld = xx.shape
+    cols = ld if cols is None else cols
+    R, C = rows - w_col + 1, cols - w_row + 1
+    vec = max(16 // x.element_size(), 1)
+    C_pad = (C + vec - 1) // vec * vec
+    if want_max and out_max is None and R > 0 and C > 0:
+        out_max = torch.empty(batch, R, C_pad, dtype=x.dtype, device=x.device)[:, :, :C]
+    if want_min and out_min is None and R > 0 and C > 0:
+        out_min = torch.empty(batch, R, C_pad, dtype=x.dtype, device=x.device)[:, :, :C]
+    om = out_max if out_max is not None else out_min
+    if om is not None and om.dim() == 2:
+        om = om[None]
+    out_ld = om.stride(1) if om is not None else 1
+    out_bs = om.stride(0) if om is not None else 1
+    _lib.check(_lib.lib().maxmin_filter_2d(dtype_code(x.dtype), _ptr(xx), batch, rows, cols,
+                                           xx.stride(1), xx.stride(0), w_row, w_col, _ptr(out_max),
+                                           _ptr(out_min), out_ld, out_bs, _stream_ptr(stream)))
+    if squeeze:
+        out_max = out_max[0] if out_max is not None and out_max.dim() == 3 else out_max
+        out_min = out_min[0] if out_min is not None and out_min.dim() == 3 else out_min
+    return out_max, out_min
+
+
+def maxmin_host_workspace_bytes(dtype, n: int, w: int, chunk: int = 0) -> int:
+    out = ctypes.c_size_t(0)
+    _lib.check(_lib.lib().maxmin_host_workspace_bytes(dtype_code(dtype), n, w, chunk, ctypes.byref(out)))
+    return int(out.value)
+
+
+def maxmin_filter_1d_host(x: torch.Tensor, w: int, out_max: torch.Tensor, out_min: torch.Tensor,
+                          dev_workspace: torch.Tensor, chunk: int = 0) -> None:
+    """End-to-end call on HOST (preferably pinned) tensors: H2D, filter, D2H inside."""
+    if x.is_cuda or out_max.is_cuda or out_min.is_cuda:
+        raise ValueError("maxmin_filter_1d_host: x/out_max/out_min must be host tensors")
+    _lib.check(_lib.lib().maxmin_filter_1d_host(dtype_code(x.dtype), _ptr(x), x.shape[0], w,
+                                                _ptr(out_max), _ptr(out_min), chunk,
+                                                _ptr(dev_workspace),
+                                                dev_workspace.numel() * dev_workspace.element_size()))

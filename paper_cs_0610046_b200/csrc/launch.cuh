@@ -1,0 +1,251 @@
+// launch.cuh -- host-side launchers (templated on the element type).  The
+// C-ABI layer (maxmin_abi.cu) validates arguments and dispatches on dtype; one
+// translation unit per dtype (inst_<t>.cu) instantiates these templates.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "k1d.cuh"
+#include "k2d.cuh"
+
+namespace mm {
+
+// status codes mirror include/maxmin.h
+enum : int { kOK = 0, kErrWorkspace = 8, kErrCuda = 9, kErrUnsupported = 10 };
+
+int note_cuda(cudaError_t e);  // records the error (thread-local), returns kErrCuda or kOK
+int sm_count();                // SMs of the current device (cached)
+
+// Tile geometry of the 1-D kernels for element type T.
+template <typename T>
+struct Geo1D {
+  static constexpr int E = Chunk<T>::E;
+  static constexpr int TILE = NT * E;
+};
+
+enum class Path1D { Copy, Small, Medium, Large };
+
+template <typename T>
+Path1D path_1d(int64_t w) {
+  if (w == 1) return Path1D::Copy;
+  if (w <= Geo1D<T>::E) return Path1D::Small;
+  if (w - 1 <= kHaloMax) return Path1D::Medium;
+  return Path1D::Large;
+}
+
+template <typename T>
+size_t workspace_1d(int64_t batch, int64_t n, int64_t w) {
+  if (path_1d<T>(w) != Path1D::Large || batch == 0) return 0;
+  const int64_t TILE = Geo1D<T>::TILE;
+  const int64_t m = n - w + 1;
+  const int64_t tpr = (m + TILE - 1) / TILE;
+  const int64_t q = (w - 1) / TILE;
+  return LargeWs<T>::bytes(batch * (q + tpr));
+}
+
+template <typename K>
+static int occupancy_grid(K kernel, size_t smem, int64_t ntiles, int &grid) {
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, NT, smem);
+  if (e != cudaSuccess) return note_cuda(e);
+  if (per_sm < 1) per_sm = 1;
+  int64_t cap = (int64_t)per_sm * sm_count();
+  grid = (int)(ntiles < cap ? ntiles : cap);
+  return kOK;
+}
+
+template <typename T, int W>
+static int launch_small(const Rows &p, cudaStream_t s) {
+  constexpr int E = Chunk<T>::E, VEC = Chunk<T>::VEC, TILE = NT * E;
+  constexpr size_t smem = sizeof(T) * 2 * (TILE + E + VEC) + 64;
+  auto kern = k1d_small<T, W>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return note_cuda(e);
+    attr = true;
+  }
+  int grid = 0;
+  int rc = occupancy_grid(kern, smem, p.ntiles, grid);
+  if (rc) return rc;
+  kern<<<grid, NT, smem, s>>>(p);
+  return note_cuda(cudaGetLastError());
+}
+
+template <typename T>
+static int launch_small_dispatch(const Rows &p, cudaStream_t s) {
+  switch (p.w) {
+    case 2: return launch_small<T, 2>(p, s);
+    case 3: return launch_small<T, 3>(p, s);
+    case 4: return launch_small<T, 4>(p, s);
+    case 5: return launch_small<T, 5>(p, s);
+    case 6: return launch_small<T, 6>(p, s);
+    case 7: return launch_small<T, 7>(p, s);
+    case 8: return launch_small<T, 8>(p, s);
+    default: break;
+  }
+  if constexpr (Chunk<T>::E == 16) {
+    switch (p.w) {
+      case 9: return launch_small<T, 9>(p, s);
+      case 10: return launch_small<T, 10>(p, s);
+      case 11: return launch_small<T, 11>(p, s);
+      case 12: return launch_small<T, 12>(p, s);
+      case 13: return launch_small<T, 13>(p, s);
+      case 14: return launch_small<T, 14>(p, s);
+      case 15: return launch_small<T, 15>(p, s);
+      case 16: return launch_small<T, 16>(p, s);
+      default: break;
+    }
+  }
+  return kErrUnsupported;
+}
+
+template <typename T>
+MedGeom medium_geom(int64_t w) {
+  constexpr int E = Chunk<T>::E;
+  int lg = 0;
+  while ((int64_t(2) << lg) <= w - 1) ++lg;  // floor(log2(w-1))
+  int lgE = 0;
+  while ((2 << lgE) <= E) ++lgE;
+  int b = lg < lgE ? lgE : lg;
+  if (b > lgE + 5) b = lgE + 5;  // B <= 32 E (one warp)
+  MedGeom g;
+  g.b = b;
+  g.q = (int)((w - 1) >> b);
+  g.r = (int)((w - 1) & ((int64_t(1) << b) - 1));
+  return g;
+}
+
+template <typename T>
+static int launch_medium(const Rows &p, cudaStream_t s) {
+  auto kern = k1d_medium<T>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)MedLayout<T>::bytes(kHaloMax + 1));
+    if (e != cudaSuccess) return note_cuda(e);
+    attr = true;
+  }
+  const size_t smem = MedLayout<T>::bytes(p.w);
+  int grid = 0;
+  int rc = occupancy_grid(kern, smem, p.ntiles, grid);
+  if (rc) return rc;
+  kern<<<grid, NT, smem, s>>>(p, medium_geom<T>(p.w));
+  return note_cuda(cudaGetLastError());
+}
+
+template <typename T>
+static int launch_large(const Rows &p, void *ws, size_t ws_bytes, cudaStream_t s) {
+  constexpr int64_t TILE = Geo1D<T>::TILE;
+  LargeGeom g;
+  g.q = (int)((p.w - 1) / TILE);
+  g.r = (int)((p.w - 1) % TILE);
+  g.tickets_per_row = g.q + p.tiles_per_row;
+  const int64_t total = p.batch * g.tickets_per_row;
+  if (!ws || ws_bytes < LargeWs<T>::bytes(total)) return kErrWorkspace;
+  if (total > 0x7fffffffLL) return kErrUnsupported;
+  cudaError_t e = cudaMemsetAsync(ws, 0, 256 + (size_t)total * 4, s);  // ticket counter + flags
+  if (e != cudaSuccess) return note_cuda(e);
+  k1d_large<T><<<(unsigned)total, NT, 0, s>>>(p, g, ws);
+  return note_cuda(cudaGetLastError());
+}
+
+// Batched 1-D filter (1-D is batch 1).  Arguments already validated.
+template <typename T>
+int launch_1d(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w, void *out_max,
+              void *out_min, int64_t out_ld, void *ws, size_t ws_bytes, cudaStream_t s) {
+  if (batch == 0) return kOK;
+  const int64_t m = n - w + 1;
+  if (w == 1) {  // identity: both outputs are copies of the input
+    for (void *o : {out_max, out_min}) {
+      if (!o) continue;
+      cudaError_t e = cudaMemcpy2DAsync(o, (size_t)out_ld * sizeof(T), in, (size_t)in_ld * sizeof(T),
+                                        (size_t)n * sizeof(T), (size_t)batch,
+                                        cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return note_cuda(e);
+    }
+    return kOK;
+  }
+  Rows p;
+  p.in = in;
+  p.out_max = out_max;
+  p.out_min = out_min;
+  p.n = n;
+  p.w = w;
+  p.m = m;
+  p.in_ld = in_ld;
+  p.out_ld = out_ld;
+  p.batch = batch;
+  p.tiles_per_row = (m + Geo1D<T>::TILE - 1) / Geo1D<T>::TILE;
+  p.ntiles = batch * p.tiles_per_row;
+  switch (path_1d<T>(w)) {
+    case Path1D::Small: return launch_small_dispatch<T>(p, s);
+    case Path1D::Medium: return launch_medium<T>(p, s);
+    case Path1D::Large: return launch_large<T>(p, ws, ws_bytes, s);
+    default: return kErrUnsupported;
+  }
+}
+
+template <typename T>
+size_t smem_2d(int64_t w_row, int64_t w_col) {
+  return K2Tile<T>::bytes((int)w_row, (int)w_col);
+}
+
+template <typename T>
+int launch_2d(const void *in, int64_t batch, int64_t rows, int64_t cols, int64_t in_ld,
+              int64_t in_bstride, int64_t w_row, int64_t w_col, void *out_max, void *out_min,
+              int64_t out_ld, int64_t out_bstride, cudaStream_t s) {
+  if (batch == 0) return kOK;
+  const size_t smem = smem_2d<T>(w_row, w_col);
+  if (smem > 200 * 1024) return kErrUnsupported;
+  auto kern = k2d_generic<T>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return note_cuda(e);
+    attr = true;
+  }
+  Img2D p;
+  p.in = in;
+  p.out_max = out_max;
+  p.out_min = out_min;
+  p.batch = batch;
+  p.rows = rows;
+  p.cols = cols;
+  p.in_ld = in_ld;
+  p.in_bstride = in_bstride;
+  p.out_ld = out_ld;
+  p.out_bstride = out_bstride;
+  p.w_row = (int)w_row;
+  p.w_col = (int)w_col;
+  const int64_t Ro = rows - w_col + 1, Co = cols - w_row + 1;
+  p.tiles_x = (Co + K2Tile<T>::TW - 1) / K2Tile<T>::TW;
+  p.tiles_y = (Ro + K2Tile<T>::TH - 1) / K2Tile<T>::TH;
+  const int64_t grid = batch * p.tiles_x * p.tiles_y;
+  if (grid > 0x7fffffffLL) return kErrUnsupported;
+  kern<<<(unsigned)grid, NT2, smem, s>>>(p);
+  return note_cuda(cudaGetLastError());
+}
+
+// Explicit instantiation declarations (definitions in inst_<t>.cu).
+#define MM_DECLARE_INST(T)                                                                     \
+  extern template int launch_1d<T>(const void *, int64_t, int64_t, int64_t, int64_t, void *,   \
+                                   void *, int64_t, void *, size_t, cudaStream_t);             \
+  extern template size_t workspace_1d<T>(int64_t, int64_t, int64_t);                          \
+  extern template int launch_2d<T>(const void *, int64_t, int64_t, int64_t, int64_t, int64_t,  \
+                                   int64_t, int64_t, void *, void *, int64_t, int64_t,         \
+                                   cudaStream_t);                                              \
+  extern template size_t smem_2d<T>(int64_t, int64_t);
+
+#define MM_DEFINE_INST(T)                                                                      \
+  template int launch_1d<T>(const void *, int64_t, int64_t, int64_t, int64_t, void *, void *,  \
+                            int64_t, void *, size_t, cudaStream_t);                            \
+  template size_t workspace_1d<T>(int64_t, int64_t, int64_t);                                  \
+  template int launch_2d<T>(const void *, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, \
+                            int64_t, void *, void *, int64_t, int64_t, cudaStream_t);          \
+  template size_t smem_2d<T>(int64_t, int64_t);
+
+}  // namespace mm

@@ -1,0 +1,332 @@
+// maxmin_abi.cu -- the C ABI of libmaxmin.so (include/maxmin.h): argument
+// validation, dtype dispatch, workspace queries and the host-buffer pipeline.
+// No compute happens here; every step of the filter runs in the kernels of
+// k1d.cuh / k2d.cuh.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/maxmin.h"
+#include "launch.cuh"
+
+namespace mm {
+
+static thread_local int g_last_cuda_error = 0;
+
+int note_cuda(cudaError_t e) {
+  if (e == cudaSuccess) return kOK;
+  g_last_cuda_error = (int)e;
+  return kErrCuda;
+}
+
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cached[dev]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    cached[dev] = v;
+  }
+  return cached[dev];
+}
+
+MM_DECLARE_INST(uint8_t)
+MM_DECLARE_INST(int8_t)
+MM_DECLARE_INST(uint16_t)
+MM_DECLARE_INST(int16_t)
+MM_DECLARE_INST(uint32_t)
+MM_DECLARE_INST(int32_t)
+MM_DECLARE_INST(uint64_t)
+MM_DECLARE_INST(int64_t)
+MM_DECLARE_INST(float)
+MM_DECLARE_INST(double)
+
+}  // namespace mm
+
+#define MM_DISPATCH(dt, CALL)                   \
+  switch (dt) {                                 \
+    case MAXMIN_U8: { using T = uint8_t; CALL; } \
+    case MAXMIN_I8: { using T = int8_t; CALL; }  \
+    case MAXMIN_U16: { using T = uint16_t; CALL; } \
+    case MAXMIN_I16: { using T = int16_t; CALL; }  \
+    case MAXMIN_U32: { using T = uint32_t; CALL; } \
+    case MAXMIN_I32: { using T = int32_t; CALL; }  \
+    case MAXMIN_U64: { using T = uint64_t; CALL; } \
+    case MAXMIN_I64: { using T = int64_t; CALL; }  \
+    case MAXMIN_F32: { using T = float; CALL; }    \
+    case MAXMIN_F64: { using T = double; CALL; }   \
+    default: return MAXMIN_ERR_DTYPE;             \
+  }
+
+namespace {
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// [lo, hi) byte ranges overlap?
+bool overlap(const void *a, size_t abytes, const void *b, size_t bbytes) {
+  uintptr_t a0 = (uintptr_t)a, a1 = a0 + abytes, b0 = (uintptr_t)b, b1 = b0 + bbytes;
+  return a0 < b1 && b0 < a1;
+}
+
+// extent in bytes of `rows` rows of `len` elements with leading dimension ld
+bool extent(int64_t rows, int64_t len, int64_t ld, size_t sz, size_t *bytes) {
+  if (rows <= 0 || len <= 0) {
+    *bytes = 0;
+    return true;
+  }
+  const int64_t lim = INT64_MAX / (int64_t)sz / 2;
+  if (ld > 0 && rows - 1 > lim / ld) return false;
+  int64_t e = (rows - 1) * ld;
+  if (e > lim - len) return false;
+  *bytes = (size_t)(e + len) * sz;
+  return true;
+}
+
+int validate_batched(int dt, const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w,
+                     const void *out_max, const void *out_min, int64_t out_ld) {
+  const size_t sz = maxmin_dtype_size(dt);
+  if (!sz) return MAXMIN_ERR_DTYPE;
+  if (!in || (!out_max && !out_min)) return MAXMIN_ERR_NULL;
+  if (w < 1) return MAXMIN_ERR_WINDOW;
+  if (n < 1 || batch < 0) return MAXMIN_ERR_SHAPE;
+  if (w > n) return MAXMIN_ERR_WINDOW_TOO_LARGE;
+  const int64_t m = n - w + 1;
+  if (in_ld < n || out_ld < m) return MAXMIN_ERR_SHAPE;
+  size_t ib, ob;
+  if (!extent(batch, n, in_ld, sz, &ib) || !extent(batch, m, out_ld, sz, &ob)) return MAXMIN_ERR_SHAPE;
+  if (!aligned16(in) || (out_max && !aligned16(out_max)) || (out_min && !aligned16(out_min)))
+    return MAXMIN_ERR_ALIGNMENT;
+  if (batch > 1 && (((size_t)in_ld * sz) % 16 != 0 || ((size_t)out_ld * sz) % 16 != 0))
+    return MAXMIN_ERR_ALIGNMENT;
+  if (batch == 0) return MAXMIN_OK;
+  if (out_max && overlap(in, ib, out_max, ob)) return MAXMIN_ERR_ALIAS;
+  if (out_min && overlap(in, ib, out_min, ob)) return MAXMIN_ERR_ALIAS;
+  if (out_max && out_min && overlap(out_max, ob, out_min, ob)) return MAXMIN_ERR_ALIAS;
+  return MAXMIN_OK;
+}
+
+// Make the device that owns `p` current for this library's runtime (the
+// caller's framework may have another device current, e.g. one rank per GPU).
+int ensure_device(const void *p) {
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return mm::note_cuda(e);
+  }
+  if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) return MAXMIN_ERR_MEMORY;
+  int cur = -1;
+  e = cudaGetDevice(&cur);
+  if (e != cudaSuccess) return mm::note_cuda(e);
+  if (cur != a.device) {
+    e = cudaSetDevice(a.device);
+    if (e != cudaSuccess) return mm::note_cuda(e);
+  }
+  return MAXMIN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *maxmin_status_str(int status) {
+  switch (status) {
+    case MAXMIN_OK: return "ok";
+    case MAXMIN_ERR_NULL: return "null pointer";
+    case MAXMIN_ERR_DTYPE: return "unknown dtype";
+    case MAXMIN_ERR_WINDOW: return "window < 1";
+    case MAXMIN_ERR_WINDOW_TOO_LARGE: return "window larger than input";
+    case MAXMIN_ERR_SHAPE: return "bad shape";
+    case MAXMIN_ERR_ALIGNMENT: return "misaligned pointer or leading dimension";
+    case MAXMIN_ERR_ALIAS: return "output overlaps input or the other output";
+    case MAXMIN_ERR_WORKSPACE: return "workspace missing or too small";
+    case MAXMIN_ERR_CUDA: return "CUDA error";
+    case MAXMIN_ERR_UNSUPPORTED: return "unsupported by this build";
+    case MAXMIN_ERR_MEMORY: return "pointer is not device memory";
+    default: return "unknown status";
+  }
+}
+
+int maxmin_last_cuda_error(void) { return mm::g_last_cuda_error; }
+
+const char *maxmin_version(void) { return "maxmin-b200 0.1 sm_100a"; }
+
+size_t maxmin_dtype_size(int dt) {
+  switch (dt) {
+    case MAXMIN_U8:
+    case MAXMIN_I8: return 1;
+    case MAXMIN_U16:
+    case MAXMIN_I16: return 2;
+    case MAXMIN_U32:
+    case MAXMIN_I32:
+    case MAXMIN_F32: return 4;
+    case MAXMIN_U64:
+    case MAXMIN_I64:
+    case MAXMIN_F64: return 8;
+    default: return 0;
+  }
+}
+
+int maxmin_workspace_bytes(int dt, int64_t batch, int64_t n, int64_t w, size_t *bytes) {
+  if (!bytes) return MAXMIN_ERR_NULL;
+  *bytes = 0;
+  if (!maxmin_dtype_size(dt)) return MAXMIN_ERR_DTYPE;
+  if (w < 1) return MAXMIN_ERR_WINDOW;
+  if (n < 1 || batch < 0) return MAXMIN_ERR_SHAPE;
+  if (w > n) return MAXMIN_ERR_WINDOW_TOO_LARGE;
+  MM_DISPATCH(dt, { *bytes = mm::workspace_1d<T>(batch, n, w); return MAXMIN_OK; })
+}
+
+int maxmin_filter_batched(int dt, const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w,
+                          void *out_max, void *out_min, int64_t out_ld, void *workspace,
+                          size_t workspace_bytes, void *stream) {
+  int rc = validate_batched(dt, in, batch, n, in_ld, w, out_max, out_min, out_ld);
+  if (rc != MAXMIN_OK) return rc;
+  size_t need = 0;
+  rc = maxmin_workspace_bytes(dt, batch, n, w, &need);
+  if (rc != MAXMIN_OK) return rc;
+  if (need > 0 && (!workspace || workspace_bytes < need || !aligned16(workspace)))
+    return MAXMIN_ERR_WORKSPACE;
+  if (need > 0) {  // the workspace must not alias the data either
+    size_t ib = 0;
+    extent(batch, n, in_ld, maxmin_dtype_size(dt), &ib);
+    if (overlap(workspace, need, in, ib)) return MAXMIN_ERR_ALIAS;
+  }
+  if (batch == 0) return MAXMIN_OK;
+  if ((rc = ensure_device(in)) != MAXMIN_OK) return rc;
+  if (out_max && (rc = ensure_device(out_max)) != MAXMIN_OK) return rc;
+  if (out_min && (rc = ensure_device(out_min)) != MAXMIN_OK) return rc;
+  if (need > 0 && (rc = ensure_device(workspace)) != MAXMIN_OK) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  MM_DISPATCH(dt, return mm::launch_1d<T>(in, batch, n, in_ld, w, out_max, out_min, out_ld,
+                                          workspace, workspace_bytes, s))
+}
+
+int maxmin_filter_1d(int dt, const void *in, int64_t n, int64_t w, void *out_max, void *out_min,
+                     void *workspace, size_t workspace_bytes, void *stream) {
+  const int64_t m = n - w + 1;
+  return maxmin_filter_batched(dt, in, 1, n, n, w, out_max, out_min, m > 0 ? m : 1, workspace,
+                               workspace_bytes, stream);
+}
+
+int maxmin_filter_2d(int dt, const void *in, int64_t batch, int64_t rows, int64_t cols, int64_t in_ld,
+                     int64_t in_bstride, int64_t w_row, int64_t w_col, void *out_max, void *out_min,
+                     int64_t out_ld, int64_t out_bstride, void *stream) {
+  const size_t sz = maxmin_dtype_size(dt);
+  if (!sz) return MAXMIN_ERR_DTYPE;
+  if (!in || (!out_max && !out_min)) return MAXMIN_ERR_NULL;
+  if (w_row < 1 || w_col < 1) return MAXMIN_ERR_WINDOW;
+  if (batch < 0 || rows < 1 || cols < 1) return MAXMIN_ERR_SHAPE;
+  if (w_row > cols || w_col > rows) return MAXMIN_ERR_WINDOW_TOO_LARGE;
+  const int64_t R = rows - w_col + 1, C = cols - w_row + 1;
+  if (in_ld < cols || out_ld < C) return MAXMIN_ERR_SHAPE;
+  if (batch > 1 && (in_bstride < rows * in_ld || out_bstride < R * out_ld)) return MAXMIN_ERR_SHAPE;
+  size_t ib, ob, t1, t2;
+  if (!extent(rows, cols, in_ld, sz, &t1) || !extent(R, C, out_ld, sz, &t2)) return MAXMIN_ERR_SHAPE;
+  if (!extent(batch, (int64_t)(t1 / sz), batch > 1 ? in_bstride : 0, sz, &ib) ||
+      !extent(batch, (int64_t)(t2 / sz), batch > 1 ? out_bstride : 0, sz, &ob))
+    return MAXMIN_ERR_SHAPE;
+  // 2-D copies each box row separately (16-B aligned outward), so only element
+  // alignment is required of pointers and strides.
+  auto el_aligned = [sz](const void *p) { return (reinterpret_cast<uintptr_t>(p) % sz) == 0; };
+  if (!el_aligned(in) || (out_max && !el_aligned(out_max)) || (out_min && !el_aligned(out_min)))
+    return MAXMIN_ERR_ALIGNMENT;
+  if (batch == 0) return MAXMIN_OK;
+  if (out_max && overlap(in, ib, out_max, ob)) return MAXMIN_ERR_ALIAS;
+  if (out_min && overlap(in, ib, out_min, ob)) return MAXMIN_ERR_ALIAS;
+  if (out_max && out_min && overlap(out_max, ob, out_min, ob)) return MAXMIN_ERR_ALIAS;
+  int rc;
+  if ((rc = ensure_device(in)) != MAXMIN_OK) return rc;
+  if (out_max && (rc = ensure_device(out_max)) != MAXMIN_OK) return rc;
+  if (out_min && (rc = ensure_device(out_min)) != MAXMIN_OK) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  MM_DISPATCH(dt, return mm::launch_2d<T>(in, batch, rows, cols, in_ld, in_bstride, w_row, w_col,
+                                          out_max, out_min, out_ld, out_bstride, s))
+}
+
+// ------------------------------------------------------------ host pipeline
+static int64_t default_chunk(int64_t chunk) { return chunk > 0 ? chunk : (int64_t(1) << 24); }
+
+int maxmin_host_workspace_bytes(int dt, int64_t n, int64_t w, int64_t chunk, size_t *bytes) {
+  if (!bytes) return MAXMIN_ERR_NULL;
+  *bytes = 0;
+  const size_t sz = maxmin_dtype_size(dt);
+  if (!sz) return MAXMIN_ERR_DTYPE;
+  if (w < 1) return MAXMIN_ERR_WINDOW;
+  if (n < 1) return MAXMIN_ERR_SHAPE;
+  if (w > n) return MAXMIN_ERR_WINDOW_TOO_LARGE;
+  const int64_t m = n - w + 1;
+  int64_t c = default_chunk(chunk);
+  if (c > m) c = m;
+  size_t ws = 0;
+  int rc = maxmin_workspace_bytes(dt, 1, c + w - 1, w, &ws);
+  if (rc) return rc;
+  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t per = up((size_t)(c + w - 1 + 16) * sz) + 2 * up((size_t)c * sz) + up(ws);
+  *bytes = 2 * per;
+  return MAXMIN_OK;
+}
+
+int maxmin_filter_1d_host(int dt, const void *in, int64_t n, int64_t w, void *out_max, void *out_min,
+                          int64_t chunk, void *dev_ws, size_t ws_bytes) {
+  const size_t sz = maxmin_dtype_size(dt);
+  if (!sz) return MAXMIN_ERR_DTYPE;
+  if (!in || (!out_max && !out_min)) return MAXMIN_ERR_NULL;
+  size_t need = 0;
+  int rc = maxmin_host_workspace_bytes(dt, n, w, chunk, &need);
+  if (rc) return rc;
+  if (!dev_ws || ws_bytes < need || !aligned16(dev_ws)) return MAXMIN_ERR_WORKSPACE;
+  if ((rc = ensure_device(dev_ws)) != MAXMIN_OK) return rc;
+  const int64_t m = n - w + 1;
+  int64_t c = default_chunk(chunk);
+  if (c > m) c = m;
+  size_t kws = 0;
+  maxmin_workspace_bytes(dt, 1, c + w - 1, w, &kws);
+  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t per = need / 2;
+  cudaStream_t st[2] = {nullptr, nullptr};
+  for (auto &s : st)
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+      rc = mm::note_cuda(cudaGetLastError());
+      break;
+    }
+  const char *hin = static_cast<const char *>(in);
+  int64_t k = 0;
+  for (int64_t j0 = 0; j0 < m && rc == MAXMIN_OK; j0 += c, ++k) {
+    const int64_t cw = m - j0 < c ? m - j0 : c;  // windows in this chunk
+    const int64_t len = cw + w - 1;              // input elements
+    char *base = static_cast<char *>(dev_ws) + (k & 1) * per;
+    char *din = base;
+    char *dmx = din + up((size_t)(c + w - 1 + 16) * sz);
+    char *dmn = dmx + up((size_t)c * sz);
+    char *dws = dmn + up((size_t)c * sz);
+    cudaStream_t s = st[k & 1];
+    cudaError_t e = cudaMemcpyAsync(din, hin + (size_t)j0 * sz, (size_t)len * sz, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) { rc = mm::note_cuda(e); break; }
+    rc = maxmin_filter_1d(dt, din, len, w, out_max ? dmx : nullptr, out_min ? dmn : nullptr,
+                          kws ? dws : nullptr, kws, s);
+    if (rc) break;
+    if (out_max) {
+      e = cudaMemcpyAsync(static_cast<char *>(out_max) + (size_t)j0 * sz, dmx, (size_t)cw * sz,
+                          cudaMemcpyDeviceToHost, s);
+      if (e != cudaSuccess) { rc = mm::note_cuda(e); break; }
+    }
+    if (out_min) {
+      e = cudaMemcpyAsync(static_cast<char *>(out_min) + (size_t)j0 * sz, dmn, (size_t)cw * sz,
+                          cudaMemcpyDeviceToHost, s);
+      if (e != cudaSuccess) { rc = mm::note_cuda(e); break; }
+    }
+  }
+  for (auto &s : st) {
+    if (!s) continue;
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess && rc == MAXMIN_OK) rc = mm::note_cuda(e);
+    cudaStreamDestroy(s);
+  }
+  return rc;
+}
+
+}  // extern "C"

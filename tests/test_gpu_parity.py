@@ -1,0 +1,263 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit for
+bit, on seeded inputs.  Sizes span several tiles and a ragged tail; every
+kernel path (copy, small, medium, large), every dtype, batched rows and 2-D
+images are covered, plus metamorphic checks that need no oracle at full size."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+mm = pytest.importorskip("paper_cs_0610046_b200")
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.dtype(f"u{a.dtype.itemsize}"))
+
+
+def assert_same(got, exp, what=""):
+    got = got.cpu().numpy() if isinstance(got, torch.Tensor) else got
+    assert got.shape == exp.shape, (what, got.shape, exp.shape)
+    g, e = bits(got), bits(exp)
+    if not np.array_equal(g, e):
+        bad = np.flatnonzero((g != e).ravel())
+        raise AssertionError(f"{what}: {bad.size} mismatches, first at {bad[0]}: "
+                             f"got {got.ravel()[bad[0]]} expected {exp.ravel()[bad[0]]}")
+
+
+def dev():
+    return torch.device("cuda:0")
+
+
+def run_1d(a, w):
+    x = torch.from_numpy(a).to(dev())
+    mx, mn = mm.maxmin_filter_1d(x, w)
+    torch.cuda.synchronize()
+    return mx, mn
+
+
+# every path and the boundaries between them (E=16 for <=4-byte types)
+W_1D = [1, 2, 3, 4, 5, 7, 8, 9, 15, 16, 17, 18, 31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256,
+        257, 511, 512, 513, 1023, 1024, 1025, 2047, 2049, 4095, 4096, 4097, 4098, 8191, 8192, 8193,
+        8194, 8195, 12289, 20000, 65536]
+
+
+@pytest.mark.parametrize("w", W_1D)
+def test_1d_f32_all_paths(cuda_device, w):
+    n = 100_003  # several tiles of 4096 + ragged tail
+    a = synth.c2(n)
+    mx, mn = run_1d(a, w)
+    ex, en, _ = oracle.appendix(a, w)
+    assert_same(mx, ex, f"max w={w}")
+    assert_same(mn, en, f"min w={w}")
+
+
+@pytest.mark.parametrize("n_minus_w", [0, 1, 2, 15, 4095, 4096, 4097])
+@pytest.mark.parametrize("w", [1, 3, 16, 17, 300, 8193, 9000])
+def test_1d_short_inputs(cuda_device, w, n_minus_w):
+    n = w + n_minus_w
+    a = synth.random_values(np.float32, n, seed=w * 7 + n_minus_w)
+    mx, mn = run_1d(a, w)
+    ex, en, _ = oracle.brute_1d(a, w) if n * w < 5e7 else oracle.appendix(a, w)
+    assert_same(mx, ex, f"max n={n} w={w}")
+    assert_same(mn, en, f"min n={n} w={w}")
+
+
+DTYPES = [np.uint8, np.int8, np.uint16, np.int16, np.uint32, np.int32, np.uint64, np.int64,
+          np.float32, np.float64]
+
+
+@pytest.mark.parametrize("dtype", DTYPES, ids=lambda d: np.dtype(d).name)
+@pytest.mark.parametrize("alphabet", [None, 5])
+def test_1d_every_dtype(cuda_device, dtype, alphabet):
+    n = 50_001
+    for k, w in enumerate([2, 3, 8, 9, 16, 17, 100, 1000, 5000, 8193, 10_000]):
+        a = synth.random_values(dtype, n, seed=1000 + k, alphabet=alphabet)
+        mx, mn = run_1d(a, w)
+        ex, en, _ = oracle.appendix(a, w)
+        assert_same(mx, ex, f"{np.dtype(dtype).name} max w={w}")
+        assert_same(mn, en, f"{np.dtype(dtype).name} min w={w}")
+
+
+def test_1d_single_output(cuda_device):
+    a = synth.c2(70_000)
+    x = torch.from_numpy(a).to(dev())
+    for w in (3, 100, 9000):
+        ex, en, _ = oracle.appendix(a, w)
+        mx, mn = mm.maxmin_filter_1d(x, w, want_min=False)
+        assert mn is None
+        assert_same(mx, ex)
+        mx, mn = mm.maxmin_filter_1d(x, w, want_max=False)
+        assert mx is None
+        assert_same(mn, en)
+
+
+def test_c1_config(cuda_device):
+    """BASELINE config C1: f64 i.i.d. U[0,1), n=100000, w=16, against brute force."""
+    a = synth.c1()
+    mx, mn = run_1d(a, 16)
+    ex, en, st = oracle.brute_1d(a, 16)
+    assert_same(mx, ex)
+    assert_same(mn, en)
+
+
+@pytest.mark.parametrize("w", [2, 17, 129, 4000, 9000])
+def test_batched_rows(cuda_device, w):
+    rows, n, ld = 37, 10_000, 10_016
+    base = synth.c3(rows=rows, length=n, ld=ld)
+    x = torch.from_numpy(base).to(dev())
+    mx, mn = mm.maxmin_filter_batched(x, w, n=n)
+    torch.cuda.synchronize()
+    ex, en = oracle.batched(base, w, n=n)
+    assert_same(mx, ex, f"batched max w={w}")
+    assert_same(mn, en, f"batched min w={w}")
+
+
+def test_c3_shape_sample(cuda_device):
+    """C3 layout [65536][4096] f32, w=129; parity on a 2048-row slice (full size in bench)."""
+    rows = 2048
+    b = synth.c3(rows=rows, row0=12345)
+    x = torch.from_numpy(b).to(dev())
+    mx, mn = mm.maxmin_filter_batched(x, 129)
+    ex, en = oracle.batched(b, 129)
+    assert_same(mx, ex)
+    assert_same(mn, en)
+
+
+@pytest.mark.parametrize("wr,wc", [(1, 1), (1, 7), (7, 1), (2, 2), (3, 5), (15, 15), (16, 16),
+                                   (17, 9), (33, 31)])
+def test_2d_u8(cuda_device, wr, wc):
+    img = synth.c4(count=3, rows=301, cols=517, nrect=10)
+    x = torch.from_numpy(img).to(dev())
+    mx, mn = mm.maxmin_filter_2d(x, wr, wc)
+    ex, en = oracle.separable_2d(img, wr, wc)
+    assert_same(mx, ex, f"2d max {wr}x{wc}")
+    assert_same(mn, en, f"2d min {wr}x{wc}")
+
+
+@pytest.mark.parametrize("dtype", DTYPES, ids=lambda d: np.dtype(d).name)
+def test_2d_every_dtype(cuda_device, dtype):
+    a = synth.random_values(dtype, 2 * 90 * 160, seed=77).reshape(2, 90, 160)
+    x = torch.from_numpy(a).to(dev())
+    for wr, wc in ((3, 4), (15, 15), (9, 1)):
+        mx, mn = mm.maxmin_filter_2d(x, wr, wc)
+        ex, en = oracle.brute_2d(a, wr, wc)
+        assert_same(mx, ex, f"2d max {wr}x{wc}")
+        assert_same(mn, en, f"2d min {wr}x{wc}")
+
+
+def test_2d_strided_output(cuda_device):
+    """C4 convention: outputs with a padded row pitch (out_ld = cols)."""
+    img = synth.c4(count=2, rows=256, cols=512, nrect=6)
+    x = torch.from_numpy(img).to(dev())
+    R, C = 256 - 14, 512 - 14
+    ox = torch.zeros(2, R, 512, dtype=torch.uint8, device=dev())
+    on = torch.zeros(2, R, 512, dtype=torch.uint8, device=dev())
+    mm.maxmin_filter_2d(x, 15, 15, out_max=ox[:, :, :C], out_min=on[:, :, :C])
+    ex, en = oracle.separable_2d(img, 15, 15)
+    assert_same(ox[:, :, :C].contiguous(), ex)
+    assert_same(on[:, :, :C].contiguous(), en)
+    assert int(ox[:, :, C:].abs().sum()) == 0  # padding untouched
+
+
+# ------------------------------------------------------------ metamorphic ---
+
+@pytest.mark.parametrize("w", [3, 32, 1024, 65536])
+def test_shift_invariance(cuda_device, w):
+    """F(a[s:]) = F(a)[s:]: moves every tile/halo seam (no oracle needed)."""
+    a = synth.c2(1 << 22)
+    x = torch.from_numpy(a).to(dev())
+    mx, mn = mm.maxmin_filter_1d(x, w)
+    for s in (4, 1000, 4096 * 3 + 8):
+        sx, sn = mm.maxmin_filter_1d(x[s:].contiguous(), w)
+        assert torch.equal(sx, mx[s:]) and torch.equal(sn, mn[s:]), s
+
+
+def test_dilation_semigroup(cuda_device):
+    """max_{w1} o max_{w2} = max_{w1+w2-1}: checks the large path against compositions."""
+    a = synth.c2(1 << 21)
+    x = torch.from_numpy(a).to(dev())
+    for w1, w2 in ((4097, 8192), (30000, 35537), (3, 65534)):
+        m1, n1 = mm.maxmin_filter_1d(x, w1)
+        m12, _ = mm.maxmin_filter_1d(m1, w2, want_min=False)
+        _, n12 = mm.maxmin_filter_1d(n1, w2, want_max=False)
+        mw, nw = mm.maxmin_filter_1d(x, w1 + w2 - 1)
+        assert torch.equal(m12, mw) and torch.equal(n12, nw), (w1, w2)
+
+
+def test_u8_complement(cuda_device):
+    a = synth.uniform_u8(5, 0, 300_000)
+    x = torch.from_numpy(a).to(dev())
+    for w in (3, 40, 10_000):
+        mx, mn = mm.maxmin_filter_1d(x, w)
+        cx, cn = mm.maxmin_filter_1d(255 - x, w)
+        assert torch.equal(mn, 255 - cx) and torch.equal(mx, 255 - cn)
+
+
+# ------------------------------------------------------------- full size ----
+
+def test_c2_full_size(cuda_device):
+    """BASELINE config C2 at full size (n = 2^28) for every window, vs the oracle."""
+    n = 1 << 28
+    a = synth.c2(n)
+    x = torch.from_numpy(a).to(dev())
+    for w in (3, 32, 1024, 65536):
+        mx, mn = mm.maxmin_filter_1d(x, w)
+        ex, en, _ = oracle.appendix(a, w)
+        assert_same(mx, ex, f"C2 max w={w}")
+        del ex
+        assert_same(mn, en, f"C2 min w={w}")
+        del mx, mn, en
+
+
+def test_c5_full_size_sampled(cuda_device):
+    """BASELINE config C5 (n = 2^30): windows around tile seams and random spots,
+    each recomputed by the oracle on the slice that contains it."""
+    n = 1 << 30
+    a = synth.c5(n)
+    x = torch.from_numpy(a).to(dev())
+    rng = np.random.default_rng(5)
+    for w in (7, 4096, 262144):
+        mx, mn = mm.maxmin_filter_1d(x, w)
+        m = n - w + 1
+        starts = [0, 4096 - 3, 4096 * 1000 - 1, m - 5000] + list(rng.integers(0, m - 5000, 6))
+        for j0 in starts:
+            j0 = int(j0)
+            k = 4096 + 37
+            sl = a[j0: j0 + k + w - 1]
+            ex, en, _ = oracle.appendix(sl, w)
+            assert_same(mx[j0: j0 + ex.shape[0]], ex, f"C5 max w={w} j0={j0}")
+            assert_same(mn[j0: j0 + en.shape[0]], en, f"C5 min w={w} j0={j0}")
+        del mx, mn
+    del x
+
+
+def test_host_pipeline(cuda_device):
+    a = synth.c2(3_000_017)
+    for w in (3, 1024, 70000):
+        ex, en, _ = oracle.appendix(a, w)
+        x = torch.from_numpy(a).pin_memory()
+        ox = torch.empty(ex.shape[0], dtype=torch.float32).pin_memory()
+        on = torch.empty(ex.shape[0], dtype=torch.float32).pin_memory()
+        chunk = 1 << 20
+        ws = torch.empty(mm.maxmin_host_workspace_bytes(torch.float32, a.shape[0], w, chunk),
+                         dtype=torch.uint8, device=dev())
+        mm.maxmin_filter_1d_host(x, w, ox, on, ws, chunk=chunk)
+        assert_same(ox.numpy(), ex)
+        assert_same(on.numpy(), en)
+
+
+def test_device_errors(cuda_device):
+    x = torch.from_numpy(synth.c2(100_000)).to(dev())
+    with pytest.raises(mm.MaxMinError) as e:
+        mm.maxmin_filter_1d(x, 70_000, workspace=torch.empty(16, dtype=torch.uint8, device=dev()))
+    assert e.value.status == 8
+    L = mm._lib.lib()
+    host = torch.zeros(1000).pin_memory()
+    out = torch.empty(998, device=dev())
+    rc = L.maxmin_filter_1d(8, host.data_ptr(), 1000, 3, out.data_ptr(), None, None, 0, None)
+    assert rc == 11  # host pointer passed to the device API
