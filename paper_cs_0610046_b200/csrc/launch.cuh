@@ -3,10 +3,13 @@
 // translation unit per dtype (inst_<t>.cu) instantiates these templates.
 #pragma once
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstddef>
 #include <cstdint>
+#include <cstring>
 
 #include "k1d.cuh"
 #include "k2d.cuh"
@@ -18,6 +21,8 @@ enum : int { kOK = 0, kErrWorkspace = 8, kErrCuda = 9, kErrUnsupported = 10 };
 
 int note_cuda(cudaError_t e);  // records the error (thread-local), returns kErrCuda or kOK
 int sm_count();                // SMs of the current device (cached)
+int encode_rows_map(CUtensorMap *map, const void *in, int elem_bytes, int64_t rows_per_series,
+                    int64_t batch, int64_t in_ld_bytes);  // maxmin_abi.cu
 
 // Tile geometry of the 1-D kernels for element type T.
 template <typename T>
@@ -57,99 +62,112 @@ static int occupancy_grid(K kernel, size_t smem, int64_t ntiles, int &grid) {
   return kOK;
 }
 
+template <typename K>
+static int set_smem(K kernel, size_t bytes, size_t &done) {
+  if (done >= bytes) return kOK;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return note_cuda(e);
+  done = bytes;
+  return kOK;
+}
+
 template <typename T, int W>
-static int launch_small(const Rows &p, cudaStream_t s) {
-  constexpr int E = Chunk<T>::E, VEC = Chunk<T>::VEC, TILE = NT * E;
-  constexpr size_t smem = sizeof(T) * 2 * (TILE + E + VEC) + 64;
+static int launch_small(const Rows &p, const CUtensorMap &map, cudaStream_t s) {
+  constexpr size_t smem = SmallLayout<T, W>::BYTES;
   auto kern = k1d_small<T, W>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return note_cuda(e);
-    attr = true;
-  }
-  int grid = 0;
-  int rc = occupancy_grid(kern, smem, p.ntiles, grid);
+  static size_t attr = 0;
+  int rc = set_smem(kern, smem, attr);
   if (rc) return rc;
-  kern<<<grid, NT, smem, s>>>(p);
+  int grid = 0;
+  rc = occupancy_grid(kern, smem, p.ntiles, grid);
+  if (rc) return rc;
+  kern<<<grid, NT, smem, s>>>(p, map);
   return note_cuda(cudaGetLastError());
 }
 
 template <typename T>
-static int launch_small_dispatch(const Rows &p, cudaStream_t s) {
+static int launch_small_dispatch(const Rows &p, const CUtensorMap &map, cudaStream_t s) {
   switch (p.w) {
-    case 2: return launch_small<T, 2>(p, s);
-    case 3: return launch_small<T, 3>(p, s);
-    case 4: return launch_small<T, 4>(p, s);
-    case 5: return launch_small<T, 5>(p, s);
-    case 6: return launch_small<T, 6>(p, s);
-    case 7: return launch_small<T, 7>(p, s);
-    case 8: return launch_small<T, 8>(p, s);
+    case 2: return launch_small<T, 2>(p, map, s);
+    case 3: return launch_small<T, 3>(p, map, s);
+    case 4: return launch_small<T, 4>(p, map, s);
+    case 5: return launch_small<T, 5>(p, map, s);
+    case 6: return launch_small<T, 6>(p, map, s);
+    case 7: return launch_small<T, 7>(p, map, s);
+    case 8: return launch_small<T, 8>(p, map, s);
     default: break;
   }
   if constexpr (Chunk<T>::E == 16) {
     switch (p.w) {
-      case 9: return launch_small<T, 9>(p, s);
-      case 10: return launch_small<T, 10>(p, s);
-      case 11: return launch_small<T, 11>(p, s);
-      case 12: return launch_small<T, 12>(p, s);
-      case 13: return launch_small<T, 13>(p, s);
-      case 14: return launch_small<T, 14>(p, s);
-      case 15: return launch_small<T, 15>(p, s);
-      case 16: return launch_small<T, 16>(p, s);
+      case 9: return launch_small<T, 9>(p, map, s);
+      case 10: return launch_small<T, 10>(p, map, s);
+      case 11: return launch_small<T, 11>(p, map, s);
+      case 12: return launch_small<T, 12>(p, map, s);
+      case 13: return launch_small<T, 13>(p, map, s);
+      case 14: return launch_small<T, 14>(p, map, s);
+      case 15: return launch_small<T, 15>(p, map, s);
+      case 16: return launch_small<T, 16>(p, map, s);
       default: break;
     }
   }
   return kErrUnsupported;
 }
 
+// Block geometry of k1d_medium: B = E*G, the largest power of two <= w-1 with
+// 1 <= G <= 32; D = w-1-B = q'B + r'.
 template <typename T>
 MedGeom medium_geom(int64_t w) {
   constexpr int E = Chunk<T>::E;
-  int lg = 0;
-  while ((int64_t(2) << lg) <= w - 1) ++lg;  // floor(log2(w-1))
-  int lgE = 0;
-  while ((2 << lgE) <= E) ++lgE;
-  int b = lg < lgE ? lgE : lg;
-  if (b > lgE + 5) b = lgE + 5;  // B <= 32 E (one warp)
+  int G = 1;
+  while (G < 32 && (int64_t)E * G * 2 <= w - 1) G *= 2;
   MedGeom g;
-  g.b = b;
-  g.q = (int)((w - 1) >> b);
-  g.r = (int)((w - 1) & ((int64_t(1) << b) - 1));
+  g.G = G;
+  g.lgG = 0;
+  while ((1 << g.lgG) < G) ++g.lgG;
+  g.B = E * G;
+  const int64_t D = w - 1 - g.B;
+  g.qp = (int)(D / g.B);
+  g.rp = (int)(D % g.B);
+  g.V = g.qp + 1;
   return g;
 }
 
 template <typename T>
-static int launch_medium(const Rows &p, cudaStream_t s) {
+static int launch_medium(const Rows &p, const CUtensorMap &map, cudaStream_t s) {
   auto kern = k1d_medium<T>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)MedLayout<T>::bytes(kHaloMax + 1));
-    if (e != cudaSuccess) return note_cuda(e);
-    attr = true;
-  }
+  static size_t attr = 0;
+  int rc = set_smem(kern, MedLayout<T>::bytes(kHaloMax + 1), attr);
+  if (rc) return rc;
   const size_t smem = MedLayout<T>::bytes(p.w);
   int grid = 0;
-  int rc = occupancy_grid(kern, smem, p.ntiles, grid);
+  rc = occupancy_grid(kern, smem, p.ntiles, grid);
   if (rc) return rc;
-  kern<<<grid, NT, smem, s>>>(p, medium_geom<T>(p.w));
+  kern<<<grid, NT, smem, s>>>(p, medium_geom<T>(p.w), map);
   return note_cuda(cudaGetLastError());
 }
 
 template <typename T>
-static int launch_large(const Rows &p, void *ws, size_t ws_bytes, cudaStream_t s) {
+static int launch_large(const Rows &p, const CUtensorMap &map, void *ws, size_t ws_bytes,
+                        cudaStream_t s) {
   constexpr int64_t TILE = Geo1D<T>::TILE;
   LargeGeom g;
   g.q = (int)((p.w - 1) / TILE);
   g.r = (int)((p.w - 1) % TILE);
   g.tickets_per_row = g.q + p.tiles_per_row;
-  const int64_t total = p.batch * g.tickets_per_row;
-  if (!ws || ws_bytes < LargeWs<T>::bytes(total)) return kErrWorkspace;
-  if (total > 0x7fffffffLL) return kErrUnsupported;
-  cudaError_t e = cudaMemsetAsync(ws, 0, 256 + (size_t)total * 4, s);  // ticket counter + flags
+  g.total = p.batch * g.tickets_per_row;
+  if (!ws || ws_bytes < LargeWs<T>::bytes(g.total)) return kErrWorkspace;
+  if (g.total > 0x7fffffffLL) return kErrUnsupported;
+  cudaError_t e = cudaMemsetAsync(ws, 0, 256 + (size_t)g.total * 4, s);  // ticket counter + flags
   if (e != cudaSuccess) return note_cuda(e);
-  k1d_large<T><<<(unsigned)total, NT, 0, s>>>(p, g, ws);
+  auto kern = k1d_large<T>;
+  constexpr size_t smem = LargeLayout<T>::BYTES;
+  static size_t attr = 0;
+  int rc = set_smem(kern, smem, attr);
+  if (rc) return rc;
+  int grid = 0;
+  rc = occupancy_grid(kern, smem, g.total, grid);
+  if (rc) return rc;
+  kern<<<grid, NT, smem, s>>>(p, g, ws, map);
   return note_cuda(cudaGetLastError());
 }
 
@@ -181,10 +199,19 @@ int launch_1d(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w
   p.batch = batch;
   p.tiles_per_row = (m + Geo1D<T>::TILE - 1) / Geo1D<T>::TILE;
   p.ntiles = batch * p.tiles_per_row;
+  // TMA map over the whole 128-B rows of every series
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  const int64_t full_rows = n / Rowing<T>::RW;
+  p.has_map = full_rows > 0 ? 1 : 0;
+  if (p.has_map) {
+    int rc = encode_rows_map(&map, in, (int)sizeof(T), full_rows, batch, in_ld * (int64_t)sizeof(T));
+    if (rc) return rc;
+  }
   switch (path_1d<T>(w)) {
-    case Path1D::Small: return launch_small_dispatch<T>(p, s);
-    case Path1D::Medium: return launch_medium<T>(p, s);
-    case Path1D::Large: return launch_large<T>(p, ws, ws_bytes, s);
+    case Path1D::Small: return launch_small_dispatch<T>(p, map, s);
+    case Path1D::Medium: return launch_medium<T>(p, map, s);
+    case Path1D::Large: return launch_large<T>(p, map, ws, ws_bytes, s);
     default: return kErrUnsupported;
   }
 }
@@ -202,12 +229,9 @@ int launch_2d(const void *in, int64_t batch, int64_t rows, int64_t cols, int64_t
   const size_t smem = smem_2d<T>(w_row, w_col);
   if (smem > 200 * 1024) return kErrUnsupported;
   auto kern = k2d_generic<T>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return note_cuda(e);
-    attr = true;
-  }
+  static size_t attr = 0;
+  int rc = set_smem(kern, 200 * 1024, attr);
+  if (rc) return rc;
   Img2D p;
   p.in = in;
   p.out_max = out_max;

@@ -33,6 +33,41 @@ int sm_count() {
   return cached[dev];
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D map {RW, rows_per_series, batch} of 128-byte rows, boxes {RW, 8, 1},
+// 128-byte swizzle, zero fill out of bounds (tma.cuh).
+int encode_rows_map(CUtensorMap *map, const void *in, int elem_bytes, int64_t rows_per_series,
+                    int64_t batch, int64_t in_ld_bytes) {
+  auto fn = encode_fn();
+  if (!fn) return note_cuda(cudaErrorNotSupported);
+  CUtensorMapDataType dt = elem_bytes == 1   ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                           : elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                           : elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32
+                                             : CU_TENSOR_MAP_DATA_TYPE_UINT64;
+  const cuuint64_t RW = 128 / elem_bytes;
+  cuuint64_t dims[3] = {RW, (cuuint64_t)rows_per_series, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {128, (cuuint64_t)(batch > 1 ? in_ld_bytes : rows_per_series * 128)};
+  cuuint32_t box[3] = {(cuuint32_t)RW, (cuuint32_t)kBoxRows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, dt, 3, const_cast<void *>(in), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return note_cuda(cudaErrorInvalidValue);
+  return kOK;
+}
+
 MM_DECLARE_INST(uint8_t)
 MM_DECLARE_INST(int8_t)
 MM_DECLARE_INST(uint16_t)
