@@ -50,6 +50,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// 1024-B aligned base inside the dynamic shared buffer.  Pointer arithmetic on
+// the __shared__ array itself (no integer round trip), so the compiler keeps
+// the shared address space and emits LDS/STS rather than generic LD/ST.
+__device__ __forceinline__ unsigned char *smem_align1024(unsigned char *raw) {
+  return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+}
+
 // Padded index: one 4-byte word (or one 8-byte element) of padding per 128 B
 // row.  Lanes that access p = base + E*lane + d (any d) then hit distinct
 // banks, for scalar accesses of every element size.

@@ -1,0 +1,284 @@
+// k1d_medium.cuh -- runtime medium-window 1-D kernel (see k1d_base.cuh).
+#pragma once
+
+#include "k1d_base.cuh"
+
+namespace mm {
+
+// ==================================================================== medium
+// Runtime w with E < w <= kHaloMax+1.  Block B = E*G (G lanes, a power of two,
+// B <= w-1; B = 32E when w-1 >= 32E).  Thread t owns the near chunk [tE, tE+E)
+// of outputs and the far chunk [tE+w-1, tE+w-1+E) of inputs; group g = t/G owns
+// near block [gB, gB+B) and far block F_g = [gB+w-1, gB+B+w-1).  With D = w-1-B
+// = q'B + r', the gap [gB+B, gB+w-1) of every window of near block g is
+//   the last r' elements of F_{g-q'-1}  and  F_{g-q'} .. F_{g-1},
+// so out = max(S_local, P_local, C_t) with C_t = max(S-carry, P-carry, gap) one
+// per-thread constant.
+//
+// Far-block aggregates (G = max of a far block, H = max of its last r'
+// elements) go to a ring indexed by the block's position in the row.  Each CTA
+// processes a contiguous range of tiles, so the far blocks "before" a tile
+// (g < 0) are the previous tile's blocks, already in the ring; only the first
+// tiles of a CTA range or of a row reduce them from the staged halo.
+struct MedGeom {
+  int G;   // lanes per block
+  int lgG;
+  int B;   // E * G
+  int qp;  // q'
+  int rp;  // r'
+  int V;   // far blocks before the tile needed by its gaps: q' + (r' > 0)
+  int need;  // previous tiles that hold those V blocks: ceil(V*G / NT)
+  int ring;  // ring entries: a power of two >= V + NT/G
+};
+
+template <typename T>
+struct MedLayout {
+  static constexpr int E = Chunk<T>::E;
+  static constexpr int TILE = NT * E;
+  static constexpr int RW = Rowing<T>::RW;
+  __host__ __device__ static int rows(int64_t w) {
+    int r = (int)((TILE + w - 1 + 16 + RW - 1) / RW);  // + margin for shifted 16-B reads
+    return (r + kBoxRows - 1) / kBoxRows * kBoxRows;
+  }
+  __host__ __device__ static size_t stage_bytes(int64_t w) { return (size_t)rows(w) * 128; }
+  __host__ __device__ static size_t bytes(int64_t w, int ring) {
+    return 1024 + 2 * stage_bytes(w) + 4 * sizeof(T) * (size_t)ring + 64;
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(NT, 2)
+    k1d_medium(Rows p, MedGeom g, const __grid_constant__ CUtensorMap map) {
+  using Lay = MedLayout<T>;
+  constexpr int E = Lay::E;
+  constexpr int TILE = Lay::TILE;
+  const int RMASK = g.ring - 1;
+  const int w = (int)p.w;
+  const size_t SB = Lay::stage_bytes(w);
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *base = smem_align1024(smem_raw);
+  auto stg = [&](int i) { return base + i * SB; };
+  T *Rgx = reinterpret_cast<T *>(base + 2 * SB);  // ring of far-block aggregates
+  T *Rgn = Rgx + g.ring;
+  T *Rhx = Rgn + g.ring;
+  T *Rhn = Rhx + g.ring;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(base + 2 * SB + 4 * sizeof(T) * g.ring);
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int G = g.G, B = g.B;
+  const int gl = lane & (G - 1);
+  const int grp = tid >> g.lgG;
+  const int gbase = lane & ~(G - 1);  // first lane of this lane's group (in the warp)
+  // H range inside a far block: block offsets [B - r', B)
+  const int hstart = B - g.rp;
+  const int h_lane = hstart / E, h_off = hstart - (hstart / E) * E;
+
+  // contiguous tile range of this CTA
+  const int64_t t_begin = p.ntiles * (int64_t)blockIdx.x / gridDim.x;
+  const int64_t t_end = p.ntiles * ((int64_t)blockIdx.x + 1) / gridDim.x;
+
+  if (tid == 0) {
+    prefetch_tmap(&map);
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0 && t_begin < t_end) {
+    int64_t row, u0;
+    int tout;
+    tile_coords<TILE>(p, t_begin, row, u0, tout);
+    stage_tile<T>(p, &map, stg(0), row, u0, tout + w - 1, &bars[0]);
+  }
+
+  // reductions / scans over the G lanes of a group (warp-uniform G)
+  auto grp_reduce = [&](T &vx, T &vn) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const int d = 1 << i;
+      if (d < G) {
+        vx = Ord<T>::mx(vx, __shfl_xor_sync(0xffffffffu, vx, d));
+        vn = Ord<T>::mn(vn, __shfl_xor_sync(0xffffffffu, vn, d));
+      }
+    }
+  };
+  // H contribution of a chunk y (block-relative chunk gl) given its local max
+  auto h_part = [&](const T (&y)[E], T ax, T an, T bl, T &hx, T &hn) {
+    hx = hn = bl;  // the block's last element: inside every non-empty H range
+    if (g.rp > 0) {
+      if (gl > h_lane) {
+        hx = Ord<T>::mx(hx, ax);
+        hn = Ord<T>::mn(hn, an);
+      } else if (gl == h_lane) {
+        T vx, vn;
+        suffix_from<T, E>(y, h_off, vx, vn);
+        hx = Ord<T>::mx(hx, vx);
+        hn = Ord<T>::mn(hn, vn);
+      }
+    }
+  };
+
+  int it = 0;
+  for (int64_t t = t_begin; t < t_end; ++t, ++it) {
+    const int st = it & 1;
+    const unsigned char *X = stg(st);
+    if (tid == 0 && t + 1 < t_end) {  // prefetch the next tile into the other stage
+      int64_t row, u0;
+      int tout;
+      tile_coords<TILE>(p, t + 1, row, u0, tout);
+      stage_tile<T>(p, &map, stg(st ^ 1), row, u0, tout + w - 1, &bars[st ^ 1]);
+    }
+    int64_t row, u0;
+    int tout;
+    tile_coords<TILE>(p, t, row, u0, tout);
+    const int64_t ab0 = u0 / B;  // far block index (within the row) of group 0
+    mbar_wait(&bars[st], (it >> 1) & 1);
+    if (patch_tail<T>(p, stg(st), row, u0, tout + w - 1, tid)) __syncthreads();
+
+    // ------------------------------------------------- far chunk: prefix
+    // ux/un end up as max(P, S) per element: local prefix of the far chunk
+    // folded with the local suffix of the near chunk (carries go into cx/cn)
+    T ux[E], un[E];
+    T cx, cn;
+    {
+      T y[E];
+      lds_swz<T, E>(X, tid * E + w - 1, y);
+      ux[0] = un[0] = y[0];
+#pragma unroll
+      for (int k = 1; k < E; ++k) {
+        ux[k] = Ord<T>::mx(ux[k - 1], y[k]);
+        un[k] = Ord<T>::mn(un[k - 1], y[k]);
+      }
+      T hx, hn;
+      h_part(y, ux[E - 1], un[E - 1], __shfl_sync(0xffffffffu, y[E - 1], gbase + G - 1), hx, hn);
+      grp_reduce(hx, hn);
+      T ax = ux[E - 1], an = un[E - 1];  // group-inclusive prefix of chunk maxima
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        const int d = 1 << i;
+        if (d < G) {
+          T vx = shfl_up(ax, d), vn = shfl_up(an, d);
+          if (gl >= d) {
+            ax = Ord<T>::mx(ax, vx);
+            an = Ord<T>::mn(an, vn);
+          }
+        }
+      }
+      cx = shfl_up(ax, 1);
+      cn = shfl_up(an, 1);
+      if (gl == 0) {  // nothing before: an element inside every window
+        cx = y[0];
+        cn = y[0];
+      }
+      if (gl == G - 1) {  // publish far block aggregates G_g, H_g
+        const int ri = (int)((ab0 + grp) & RMASK);
+        Rgx[ri] = ax;
+        Rgn[ri] = an;
+        Rhx[ri] = hx;
+        Rhn[ri] = hn;
+      }
+    }
+
+    // ------------------------------------------------ near chunk: suffix
+    {
+      T x[E];
+      lds_swz_aligned<T, E>(X, tid * E, x);
+      T sx = x[E - 1], sn = x[E - 1];
+      ux[E - 1] = Ord<T>::mx(ux[E - 1], sx);
+      un[E - 1] = Ord<T>::mn(un[E - 1], sn);
+#pragma unroll
+      for (int k = E - 2; k >= 0; --k) {
+        sx = Ord<T>::mx(sx, x[k]);
+        sn = Ord<T>::mn(sn, x[k]);
+        ux[k] = Ord<T>::mx(ux[k], sx);
+        un[k] = Ord<T>::mn(un[k], sn);
+      }
+      T bx = sx, bn = sn;  // group-inclusive suffix of chunk maxima
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        const int d = 1 << i;
+        if (d < G) {
+          T dx = shfl_down(bx, d), dn = shfl_down(bn, d);
+          if (gl + d < G) {
+            bx = Ord<T>::mx(bx, dx);
+            bn = Ord<T>::mn(bn, dn);
+          }
+        }
+      }
+      T ex = shfl_down(bx, 1), en = shfl_down(bn, 1);
+      if (gl == G - 1) {  // nothing after: an element inside every window of the chunk
+        ex = x[E - 1];
+        en = x[E - 1];
+      }
+      cx = Ord<T>::mx(cx, ex);
+      cn = Ord<T>::mn(cn, en);
+    }
+
+    // ---------------- far blocks before the tile (first tiles of a range/row)
+    const int64_t tile_in_row = u0 / TILE;
+    if (g.V > 0 && (t - t_begin < g.need || tile_in_row < g.need)) {
+      const int nv = g.V * G;  // chunks of the V blocks
+      for (int r0 = 0; r0 < nv; r0 += NT) {
+        const int vc = r0 + tid;
+        if (r0 + (tid & ~31) >= nv) break;  // whole warp idle (warp-uniform)
+        const int vcc = vc < nv ? vc : nv - 1;
+        const int gv = vcc >> g.lgG;  // 0 .. V-1  <->  g' = gv - V
+        const int pos = (gv - g.V) * B + w - 1 + gl * E;
+        T y[E];
+        lds_swz<T, E>(X, pos, y);
+        T ax = y[0], an = y[0];
+#pragma unroll
+        for (int k = 1; k < E; ++k) {
+          ax = Ord<T>::mx(ax, y[k]);
+          an = Ord<T>::mn(an, y[k]);
+        }
+        T hx, hn;
+        h_part(y, ax, an, __shfl_sync(0xffffffffu, y[E - 1], gbase + G - 1), hx, hn);
+        grp_reduce(ax, an);
+        grp_reduce(hx, hn);
+        if (vc < nv && gl == 0) {
+          const int ri = (int)((ab0 + gv - g.V) & RMASK);
+          Rgx[ri] = ax;
+          Rgn[ri] = an;
+          Rhx[ri] = hx;
+          Rhn[ri] = hn;
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---------------------------------------------------------- gap + out
+    if (g.qp > 0 || g.rp > 0) {
+      const int64_t b0 = ab0 + grp - g.qp - 1;  // far block F_{g-q'-1}
+      T mx, mn;
+      if (g.rp > 0) {
+        mx = Rhx[b0 & RMASK];
+        mn = Rhn[b0 & RMASK];
+      } else {
+        mx = Rgx[(b0 + 1) & RMASK];
+        mn = Rgn[(b0 + 1) & RMASK];
+      }
+      for (int s = 1; s <= g.qp; ++s) {
+        mx = Ord<T>::mx(mx, Rgx[(b0 + s) & RMASK]);
+        mn = Ord<T>::mn(mn, Rgn[(b0 + s) & RMASK]);
+      }
+      cx = Ord<T>::mx(cx, mx);
+      cn = Ord<T>::mn(cn, mn);
+    }
+    const int c0 = tid * E;
+    if (c0 < tout) {
+      T ox[E], on[E];
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        ox[k] = Ord<T>::mx(ux[k], cx);
+        on[k] = Ord<T>::mn(un[k], cn);
+      }
+      store_out<T, E>(p, row, u0 + c0, tout - c0, ox, on);
+    }
+    __syncthreads();  // stage st and the ring reads are done before the next tile
+  }
+}
+
+}  // namespace mm

@@ -128,7 +128,10 @@ MedGeom medium_geom(int64_t w) {
   const int64_t D = w - 1 - g.B;
   g.qp = (int)(D / g.B);
   g.rp = (int)(D % g.B);
-  g.V = g.qp + 1;
+  g.V = g.qp + (g.rp > 0 ? 1 : 0);
+  g.need = (g.V * G + NT - 1) / NT;
+  g.ring = 1;
+  while (g.ring < g.V + NT / G) g.ring *= 2;
   return g;
 }
 
@@ -136,13 +139,14 @@ template <typename T>
 static int launch_medium(const Rows &p, const CUtensorMap &map, cudaStream_t s) {
   auto kern = k1d_medium<T>;
   static size_t attr = 0;
-  int rc = set_smem(kern, MedLayout<T>::bytes(kHaloMax + 1), attr);
+  const MedGeom g = medium_geom<T>(p.w);
+  const size_t smem = MedLayout<T>::bytes(p.w, g.ring);
+  int rc = set_smem(kern, smem, attr);
   if (rc) return rc;
-  const size_t smem = MedLayout<T>::bytes(p.w);
   int grid = 0;
   rc = occupancy_grid(kern, smem, p.ntiles, grid);
   if (rc) return rc;
-  kern<<<grid, NT, smem, s>>>(p, medium_geom<T>(p.w), map);
+  kern<<<grid, NT, smem, s>>>(p, g, map);
   return note_cuda(cudaGetLastError());
 }
 
@@ -157,7 +161,7 @@ static int launch_large(const Rows &p, const CUtensorMap &map, void *ws, size_t 
   g.total = p.batch * g.tickets_per_row;
   if (!ws || ws_bytes < LargeWs<T>::bytes(g.total)) return kErrWorkspace;
   if (g.total > 0x7fffffffLL) return kErrUnsupported;
-  cudaError_t e = cudaMemsetAsync(ws, 0, 256 + (size_t)g.total * 4, s);  // ticket counter + flags
+  cudaError_t e = cudaMemsetAsync(ws, 0, LargeWs<T>::zero_bytes(g.total), s);  // counter + flags
   if (e != cudaSuccess) return note_cuda(e);
   auto kern = k1d_large<T>;
   constexpr size_t smem = LargeLayout<T>::BYTES;
