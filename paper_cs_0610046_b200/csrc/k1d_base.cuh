@@ -61,6 +61,33 @@ __device__ __forceinline__ void tile_coords(const Rows &p, int64_t t, int64_t &r
   tout = left < TILE ? (int)left : TILE;
 }
 
+// Position of a tile, advanced incrementally (no 64-bit division per tile).
+template <int TILE>
+struct TileCursor {
+  int64_t row, u0;
+  __device__ __forceinline__ void start(const Rows &p, int64_t t) {
+    row = t / p.tiles_per_row;
+    u0 = (t - row * p.tiles_per_row) * (int64_t)TILE;
+  }
+  __device__ __forceinline__ void advance(const Rows &p) {
+    u0 += TILE;
+    if (u0 >= p.m) {
+      u0 = 0;
+      ++row;
+    }
+  }
+  __device__ __forceinline__ int tout(const Rows &p) const {
+    const int64_t left = p.m - u0;
+    return left < TILE ? (int)left : TILE;
+  }
+};
+
+// Contiguous, balanced range [t_begin, t_end) of tiles for this CTA.
+__device__ __forceinline__ void cta_tile_range(const Rows &p, int64_t &t_begin, int64_t &t_end) {
+  t_begin = p.ntiles * (int64_t)blockIdx.x / gridDim.x;
+  t_end = p.ntiles * ((int64_t)blockIdx.x + 1) / gridDim.x;
+}
+
 template <typename T>
 __device__ __forceinline__ const T *series_ptr(const Rows &p, int64_t row) {
   return static_cast<const T *>(p.in) + row * p.in_ld;

@@ -20,15 +20,14 @@ namespace mm {
 // processes a contiguous range of tiles, so the far blocks "before" a tile
 // (g < 0) are the previous tile's blocks, already in the ring; only the first
 // tiles of a CTA range or of a row reduce them from the staged halo.
+// G is a template parameter: the group scans unroll without branches.
 struct MedGeom {
-  int G;   // lanes per block
-  int lgG;
-  int B;   // E * G
-  int qp;  // q'
-  int rp;  // r'
-  int V;   // far blocks before the tile needed by its gaps: q' + (r' > 0)
+  int B;     // E * G
+  int qp;    // q'
+  int rp;    // r'
+  int V;     // far blocks before the tile needed by its gaps: q' + (r' > 0)
   int need;  // previous tiles that hold those V blocks: ceil(V*G / NT)
-  int ring;  // ring entries: a power of two >= V + NT/G
+  int ring;  // ring entries: a power of two >= V + 2*NT/G
 };
 
 template <typename T>
@@ -46,12 +45,46 @@ struct MedLayout {
   }
 };
 
-template <typename T>
+// inclusive max/min scans and reductions over aligned groups of G lanes
+template <typename T, int G>
+__device__ __forceinline__ void grp_reduce(T &vx, T &vn) {
+#pragma unroll
+  for (int d = 1; d < G; d <<= 1) {
+    vx = Ord<T>::mx(vx, __shfl_xor_sync(0xffffffffu, vx, d));
+    vn = Ord<T>::mn(vn, __shfl_xor_sync(0xffffffffu, vn, d));
+  }
+}
+template <typename T, int G>
+__device__ __forceinline__ void grp_scan_up(T &vx, T &vn, int gl) {
+#pragma unroll
+  for (int d = 1; d < G; d <<= 1) {
+    const T ux = shfl_up(vx, d), un = shfl_up(vn, d);
+    if (gl >= d) {
+      vx = Ord<T>::mx(vx, ux);
+      vn = Ord<T>::mn(vn, un);
+    }
+  }
+}
+template <typename T, int G>
+__device__ __forceinline__ void grp_scan_down(T &vx, T &vn, int gl) {
+#pragma unroll
+  for (int d = 1; d < G; d <<= 1) {
+    const T ux = shfl_down(vx, d), un = shfl_down(vn, d);
+    if (gl + d < G) {
+      vx = Ord<T>::mx(vx, ux);
+      vn = Ord<T>::mn(vn, un);
+    }
+  }
+}
+
+template <typename T, int G>
 __global__ void __launch_bounds__(NT, 2)
     k1d_medium(Rows p, MedGeom g, const __grid_constant__ CUtensorMap map) {
   using Lay = MedLayout<T>;
   constexpr int E = Lay::E;
   constexpr int TILE = Lay::TILE;
+  constexpr int B = E * G;
+  constexpr int NG = NT / G;  // groups per tile
   const int RMASK = g.ring - 1;
   const int w = (int)p.w;
   const size_t SB = Lay::stage_bytes(w);
@@ -67,17 +100,18 @@ __global__ void __launch_bounds__(NT, 2)
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
-  const int G = g.G, B = g.B;
   const int gl = lane & (G - 1);
-  const int grp = tid >> g.lgG;
-  const int gbase = lane & ~(G - 1);  // first lane of this lane's group (in the warp)
+  const int grp = tid / G;
+  const int glast = (lane & ~(G - 1)) + G - 1;  // last lane of this lane's group
   // H range inside a far block: block offsets [B - r', B)
   const int hstart = B - g.rp;
   const int h_lane = hstart / E, h_off = hstart - (hstart / E) * E;
 
-  // contiguous tile range of this CTA
-  const int64_t t_begin = p.ntiles * (int64_t)blockIdx.x / gridDim.x;
-  const int64_t t_end = p.ntiles * ((int64_t)blockIdx.x + 1) / gridDim.x;
+  int64_t t_begin, t_end;
+  cta_tile_range(p, t_begin, t_end);
+  TileCursor<TILE> cur, nxt;
+  cur.start(p, t_begin);
+  nxt = cur;
 
   if (tid == 0) {
     prefetch_tmap(&map);
@@ -86,24 +120,9 @@ __global__ void __launch_bounds__(NT, 2)
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0 && t_begin < t_end) {
-    int64_t row, u0;
-    int tout;
-    tile_coords<TILE>(p, t_begin, row, u0, tout);
-    stage_tile<T>(p, &map, stg(0), row, u0, tout + w - 1, &bars[0]);
-  }
+  if (tid == 0 && t_begin < t_end)
+    stage_tile<T>(p, &map, stg(0), cur.row, cur.u0, cur.tout(p) + w - 1, &bars[0]);
 
-  // reductions / scans over the G lanes of a group (warp-uniform G)
-  auto grp_reduce = [&](T &vx, T &vn) {
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      const int d = 1 << i;
-      if (d < G) {
-        vx = Ord<T>::mx(vx, __shfl_xor_sync(0xffffffffu, vx, d));
-        vn = Ord<T>::mn(vn, __shfl_xor_sync(0xffffffffu, vn, d));
-      }
-    }
-  };
   // H contribution of a chunk y (block-relative chunk gl) given its local max
   auto h_part = [&](const T (&y)[E], T ax, T an, T bl, T &hx, T &hn) {
     hx = hn = bl;  // the block's last element: inside every non-empty H range
@@ -124,15 +143,11 @@ __global__ void __launch_bounds__(NT, 2)
   for (int64_t t = t_begin; t < t_end; ++t, ++it) {
     const int st = it & 1;
     const unsigned char *X = stg(st);
-    if (tid == 0 && t + 1 < t_end) {  // prefetch the next tile into the other stage
-      int64_t row, u0;
-      int tout;
-      tile_coords<TILE>(p, t + 1, row, u0, tout);
-      stage_tile<T>(p, &map, stg(st ^ 1), row, u0, tout + w - 1, &bars[st ^ 1]);
-    }
-    int64_t row, u0;
-    int tout;
-    tile_coords<TILE>(p, t, row, u0, tout);
+    nxt.advance(p);
+    if (tid == 0 && t + 1 < t_end)  // prefetch the next tile into the other stage
+      stage_tile<T>(p, &map, stg(st ^ 1), nxt.row, nxt.u0, nxt.tout(p) + w - 1, &bars[st ^ 1]);
+    const int64_t row = cur.row, u0 = cur.u0;
+    const int tout = cur.tout(p);
     const int64_t ab0 = u0 / B;  // far block index (within the row) of group 0
     mbar_wait(&bars[st], (it >> 1) & 1);
     if (patch_tail<T>(p, stg(st), row, u0, tout + w - 1, tid)) __syncthreads();
@@ -152,20 +167,10 @@ __global__ void __launch_bounds__(NT, 2)
         un[k] = Ord<T>::mn(un[k - 1], y[k]);
       }
       T hx, hn;
-      h_part(y, ux[E - 1], un[E - 1], __shfl_sync(0xffffffffu, y[E - 1], gbase + G - 1), hx, hn);
-      grp_reduce(hx, hn);
+      h_part(y, ux[E - 1], un[E - 1], __shfl_sync(0xffffffffu, y[E - 1], glast), hx, hn);
+      grp_reduce<T, G>(hx, hn);
       T ax = ux[E - 1], an = un[E - 1];  // group-inclusive prefix of chunk maxima
-#pragma unroll
-      for (int i = 0; i < 5; ++i) {
-        const int d = 1 << i;
-        if (d < G) {
-          T vx = shfl_up(ax, d), vn = shfl_up(an, d);
-          if (gl >= d) {
-            ax = Ord<T>::mx(ax, vx);
-            an = Ord<T>::mn(an, vn);
-          }
-        }
-      }
+      grp_scan_up<T, G>(ax, an, gl);
       cx = shfl_up(ax, 1);
       cn = shfl_up(an, 1);
       if (gl == 0) {  // nothing before: an element inside every window
@@ -196,17 +201,7 @@ __global__ void __launch_bounds__(NT, 2)
         un[k] = Ord<T>::mn(un[k], sn);
       }
       T bx = sx, bn = sn;  // group-inclusive suffix of chunk maxima
-#pragma unroll
-      for (int i = 0; i < 5; ++i) {
-        const int d = 1 << i;
-        if (d < G) {
-          T dx = shfl_down(bx, d), dn = shfl_down(bn, d);
-          if (gl + d < G) {
-            bx = Ord<T>::mx(bx, dx);
-            bn = Ord<T>::mn(bn, dn);
-          }
-        }
-      }
+      grp_scan_down<T, G>(bx, bn, gl);
       T ex = shfl_down(bx, 1), en = shfl_down(bn, 1);
       if (gl == G - 1) {  // nothing after: an element inside every window of the chunk
         ex = x[E - 1];
@@ -224,7 +219,7 @@ __global__ void __launch_bounds__(NT, 2)
         const int vc = r0 + tid;
         if (r0 + (tid & ~31) >= nv) break;  // whole warp idle (warp-uniform)
         const int vcc = vc < nv ? vc : nv - 1;
-        const int gv = vcc >> g.lgG;  // 0 .. V-1  <->  g' = gv - V
+        const int gv = vcc / G;  // 0 .. V-1  <->  g' = gv - V
         const int pos = (gv - g.V) * B + w - 1 + gl * E;
         T y[E];
         lds_swz<T, E>(X, pos, y);
@@ -235,9 +230,9 @@ __global__ void __launch_bounds__(NT, 2)
           an = Ord<T>::mn(an, y[k]);
         }
         T hx, hn;
-        h_part(y, ax, an, __shfl_sync(0xffffffffu, y[E - 1], gbase + G - 1), hx, hn);
-        grp_reduce(ax, an);
-        grp_reduce(hx, hn);
+        h_part(y, ax, an, __shfl_sync(0xffffffffu, y[E - 1], glast), hx, hn);
+        grp_reduce<T, G>(ax, an);
+        grp_reduce<T, G>(hx, hn);
         if (vc < nv && gl == 0) {
           const int ri = (int)((ab0 + gv - g.V) & RMASK);
           Rgx[ri] = ax;
@@ -277,8 +272,16 @@ __global__ void __launch_bounds__(NT, 2)
       }
       store_out<T, E>(p, row, u0 + c0, tout - c0, ox, on);
     }
-    __syncthreads();  // stage st and the ring reads are done before the next tile
+    // No barrier needed before the next tile in steady state: stage st was last
+    // read before this tile's barrier (the prefetch into it is issued after it),
+    // and the ring holds >= V + 2*NT/G entries, so the next tile's writes never
+    // alias this tile's reads.  A fresh next tile rewrites the V entries before
+    // it: wait for this tile's readers first.
+    if (t + 1 < t_end && g.V > 0 && (t + 1 - t_begin < g.need || nxt.u0 / TILE < g.need))
+      __syncthreads();
+    cur = nxt;
   }
+  (void)NG;
 }
 
 }  // namespace mm

@@ -43,26 +43,22 @@ __global__ void __launch_bounds__(NT) k1d_small(Rows p, const __grid_constant__ 
     fence_mbar_init();
   }
   __syncthreads();
-  const int64_t grid = gridDim.x;
-  if (tid == 0 && (int64_t)blockIdx.x < p.ntiles) {
-    int64_t row, u0;
-    int tout;
-    tile_coords<TILE>(p, blockIdx.x, row, u0, tout);
-    stage_tile<T>(p, &map, stg(0), row, u0, tout + W - 1, &bars[0]);
-  }
+  int64_t t_begin, t_end;
+  cta_tile_range(p, t_begin, t_end);
+  TileCursor<TILE> cur, nxt;
+  cur.start(p, t_begin);
+  nxt = cur;
+  if (tid == 0 && t_begin < t_end)
+    stage_tile<T>(p, &map, stg(0), cur.row, cur.u0, cur.tout(p) + W - 1, &bars[0]);
   int it = 0;
-  for (int64_t t = blockIdx.x; t < p.ntiles; t += grid, ++it) {
+  for (int64_t t = t_begin; t < t_end; ++t, ++it, cur = nxt) {
     const int st = it & 1;
     unsigned char *X = stg(st);
-    if (tid == 0 && t + grid < p.ntiles) {  // prefetch the next tile into the other stage
-      int64_t row, u0;
-      int tout;
-      tile_coords<TILE>(p, t + grid, row, u0, tout);
-      stage_tile<T>(p, &map, stg(st ^ 1), row, u0, tout + W - 1, &bars[st ^ 1]);
-    }
-    int64_t row, u0;
-    int tout;
-    tile_coords<TILE>(p, t, row, u0, tout);
+    nxt.advance(p);
+    if (tid == 0 && t + 1 < t_end)  // prefetch the next tile into the other stage
+      stage_tile<T>(p, &map, stg(st ^ 1), nxt.row, nxt.u0, nxt.tout(p) + W - 1, &bars[st ^ 1]);
+    const int64_t row = cur.row, u0 = cur.u0;
+    const int tout = cur.tout(p);
     mbar_wait(&bars[st], (it >> 1) & 1);
     if (patch_tail<T>(p, X, row, u0, tout + W - 1, tid)) __syncthreads();
 

@@ -115,15 +115,20 @@ static int launch_small_dispatch(const Rows &p, const CUtensorMap &map, cudaStre
 
 // Block geometry of k1d_medium: B = E*G, the largest power of two <= w-1 with
 // 1 <= G <= 32; D = w-1-B = q'B + r'.
+// Lanes per block of k1d_medium: the largest power of two G <= 32 with E*G <= w-1.
 template <typename T>
-MedGeom medium_geom(int64_t w) {
+int medium_G(int64_t w) {
   constexpr int E = Chunk<T>::E;
   int G = 1;
   while (G < 32 && (int64_t)E * G * 2 <= w - 1) G *= 2;
+  return G;
+}
+
+// Block geometry of k1d_medium: B = E*G; D = w-1-B = q'B + r'.
+template <typename T>
+MedGeom medium_geom(int64_t w, int G) {
+  constexpr int E = Chunk<T>::E;
   MedGeom g;
-  g.G = G;
-  g.lgG = 0;
-  while ((1 << g.lgG) < G) ++g.lgG;
   g.B = E * G;
   const int64_t D = w - 1 - g.B;
   g.qp = (int)(D / g.B);
@@ -131,15 +136,15 @@ MedGeom medium_geom(int64_t w) {
   g.V = g.qp + (g.rp > 0 ? 1 : 0);
   g.need = (g.V * G + NT - 1) / NT;
   g.ring = 1;
-  while (g.ring < g.V + NT / G) g.ring *= 2;
+  while (g.ring < g.V + 2 * (NT / G)) g.ring *= 2;
   return g;
 }
 
-template <typename T>
-static int launch_medium(const Rows &p, const CUtensorMap &map, cudaStream_t s) {
-  auto kern = k1d_medium<T>;
+template <typename T, int G>
+static int launch_medium_g(const Rows &p, const CUtensorMap &map, cudaStream_t s) {
+  auto kern = k1d_medium<T, G>;
   static size_t attr = 0;
-  const MedGeom g = medium_geom<T>(p.w);
+  const MedGeom g = medium_geom<T>(p.w, G);
   const size_t smem = MedLayout<T>::bytes(p.w, g.ring);
   int rc = set_smem(kern, smem, attr);
   if (rc) return rc;
@@ -148,6 +153,18 @@ static int launch_medium(const Rows &p, const CUtensorMap &map, cudaStream_t s) 
   if (rc) return rc;
   kern<<<grid, NT, smem, s>>>(p, g, map);
   return note_cuda(cudaGetLastError());
+}
+
+template <typename T>
+static int launch_medium(const Rows &p, const CUtensorMap &map, cudaStream_t s) {
+  switch (medium_G<T>(p.w)) {
+    case 1: return launch_medium_g<T, 1>(p, map, s);
+    case 2: return launch_medium_g<T, 2>(p, map, s);
+    case 4: return launch_medium_g<T, 4>(p, map, s);
+    case 8: return launch_medium_g<T, 8>(p, map, s);
+    case 16: return launch_medium_g<T, 16>(p, map, s);
+    default: return launch_medium_g<T, 32>(p, map, s);
+  }
 }
 
 template <typename T>
