@@ -15,12 +15,16 @@ namespace mm {
 // whole F_{x-q+1} .. F_{x-1}.  Every tile publishes G_x = max F_x and H_x = max
 // of the last r elements of F_x; tile x consumes H_{x-q}, G_{x-q+1..x-1}.
 // Tiles x in [-q, -1] exist only to publish (their F lies inside the array).
+//
 // Tickets (atomic counter) order the tiles: ticket = (row, x+q) row-major, so
 // the look-back distance is q tiles of the global stream and F_x is still in L2
-// when tile x+q stages it as its near tile.  A CTA publishes before it waits and
-// waits only on lower tickets; a CTA holding a prefetched next ticket finishes
-// its current one (which only waits on lower tickets) first -- deadlock-free for
-// any number of resident CTAs.
+// when tile x+q stages it as its near tile.  Each CTA runs a 3-stage TMA ring:
+// in iteration i it (1) grabs and stages ticket i+2, (2) publishes the
+// aggregates of ticket i+1 (already staged), (3) processes ticket i, whose
+// predecessors were published an iteration earlier -- the look-back normally
+// finds its values ready and stays off the critical path.  Publishing waits on
+// nothing but TMA data and waits only target lower tickets, so the scheme is
+// deadlock-free for any number of resident CTAs.
 //
 // Publication: for element types of <= 4 bytes each aggregate travels as one
 // 64-bit word (1 << 32 | bits), written and polled with relaxed gpu-scope
@@ -52,11 +56,12 @@ struct LargeLayout {
   static constexpr int E = Chunk<T>::E;
   static constexpr int TILE = NT * E;
   static constexpr int RW = Rowing<T>::RW;
+  static constexpr int NSTAGE = 3;
   static constexpr int NROWS = (TILE / RW + kBoxRows - 1) / kBoxRows * kBoxRows;
   static constexpr int FROWS = ((TILE + RW) / RW + kBoxRows - 1) / kBoxRows * kBoxRows;
   static constexpr size_t NB = (size_t)NROWS * 128, FB = (size_t)FROWS * 128;
   static constexpr size_t STAGE = NB + FB;
-  static constexpr size_t BYTES = 1024 + 2 * STAGE + 256;
+  static constexpr size_t BYTES = 1024 + NSTAGE * STAGE + 256;
 };
 
 template <typename T>
@@ -90,15 +95,19 @@ __global__ void __launch_bounds__(NT, 2)
   constexpr int E = Lay::E;
   constexpr int TILE = Lay::TILE;
   constexpr int RW = Lay::RW;
+  constexpr int NS = Lay::NSTAGE;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *base = smem_align1024(smem_raw);
   auto nearb = [&](int i) { return base + i * Lay::STAGE; };
   auto farb = [&](int i) { return base + i * Lay::STAGE + Lay::NB; };
-  __shared__ T wagg[4][NWARP];
-  __shared__ int64_t s_ticket[2];
-  __shared__ int s_fshift[2];
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ T wpub[2][4][NWARP];  // G/H partials of the published ticket (by parity)
+  __shared__ T wpre[2][NWARP];     // far prefix warp totals of the processed ticket
+  __shared__ T wsuf[2][NWARP];     // near suffix warp totals
+  __shared__ T wgap[2][NWARP];     // look-back gap partials
+  __shared__ int64_t s_ticket[NS];
+  __shared__ int s_fshift[NS];
+  __shared__ __align__(8) uint64_t bars[NS];
 
   unsigned long long *counter = reinterpret_cast<unsigned long long *>(ws);
   uint32_t *flags = reinterpret_cast<uint32_t *>(static_cast<char *>(ws) + 256);  // 8-B types
@@ -108,18 +117,25 @@ __global__ void __launch_bounds__(NT, 2)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t w = p.w;
 
-  // stage ticket tk into stage st (thread 0 only)
-  auto stage_ticket = [&](int64_t tk, int st) {
+  auto decode = [&](int64_t tk, int64_t &row, int64_t &x) {
+    row = tk / g.tickets_per_row;
+    x = tk - row * g.tickets_per_row - g.q;  // may be negative
+  };
+
+  // grab a ticket and stage it into stage st (thread 0 only)
+  auto stage_ticket = [&](int st) {
+    const int64_t tk = (int64_t)atomicAdd(counter, 1ull);
     s_ticket[st] = tk;
     if (tk >= g.total) {
       mbar_arrive_expect_tx(&bars[st], 0);
       return;
     }
-    const int64_t row = tk / g.tickets_per_row;
-    const int64_t x = tk - row * g.tickets_per_row - g.q;
+    int64_t row, x;
+    decode(tk, row, x);
     const int64_t u0 = x * TILE;
     const int64_t f0 = u0 + w - 1;
     const int64_t flen = p.n - f0 < TILE ? p.n - f0 : TILE;
+    s_fshift[st] = (int)(f0 - (f0 / RW) * RW);
     if (p.has_map) {
       const int64_t fr0 = f0 / RW, fr1 = (f0 + flen + RW - 1) / RW;
       const int nfb = (int)((fr1 - fr0 + kBoxRows - 1) / kBoxRows);
@@ -132,60 +148,161 @@ __global__ void __launch_bounds__(NT, 2)
     } else {
       mbar_arrive_expect_tx(&bars[st], 0);
     }
-    s_fshift[st] = (int)(f0 - (f0 / RW) * RW);
   };
 
-  if (tid == 0) {
-    prefetch_tmap(&map);
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
-    stage_ticket((int64_t)atomicAdd(counter, 1ull), 0);
-  }
-  __syncthreads();
-
-  for (int it = 0;; ++it) {
-    const int st = it & 1;
-    const int64_t ticket = s_ticket[st];
-    if (ticket >= g.total) break;
-    if (tid == 0)  // prefetch the next ticket into the other stage
-      stage_ticket((int64_t)atomicAdd(counter, 1ull), st ^ 1);
-    const int64_t row = ticket / g.tickets_per_row;
-    const int64_t x = ticket - row * g.tickets_per_row - g.q;  // may be negative
+  // after the stage's barrier: patch the partial last 128-B row (all threads);
+  // returns whether shared memory was written
+  auto patch = [&](int st, int64_t row, int64_t x) -> bool {
+    const int64_t full = p.has_map ? (p.n / RW) * RW : 0;
+    if (full >= p.n) return false;
+    bool fixed = false;
+    const T *srs = series_ptr<T>(p, row);
     const int64_t u0 = x * TILE;
     const int64_t f0 = u0 + w - 1;
-    int tout = 0;
-    if (x >= 0) {
+    const int64_t fa = f0 - s_fshift[st];  // absolute start of the far stage
+    const int64_t fe = f0 + TILE;
+    if (full < fe && p.n > fa) {
+      const int64_t lo = full > fa ? full : fa, hi = p.n < fe ? p.n : fe;
+      for (int64_t i = lo + tid; i < hi; i += NT) sts_swz<T>(farb(st), (int)(i - fa), srs[i]);
+      fixed = true;
+    }
+    if (x >= 0 && full < u0 + TILE && p.n > u0) {
+      const int64_t lo = full > u0 ? full : u0, hi = p.n < u0 + TILE ? p.n : u0 + TILE;
+      for (int64_t i = lo + tid; i < hi; i += NT) sts_swz<T>(nearb(st), (int)(i - u0), srs[i]);
+      fixed = true;
+    }
+    return fixed;
+  };
+
+  // Publish G/H of the ticket staged for iteration `itp` (all threads).  Always
+  // ends with one barrier, which also fences the process-step partials.
+  auto publish = [&](int itp) {
+    const int st = itp % NS;
+    const int pb = itp & 1;
+    const int64_t tk = s_ticket[st];
+    if (tk >= g.total) {  // uniform
+      __syncthreads();
+      return;
+    }
+    int64_t row, x;
+    decode(tk, row, x);
+    mbar_wait(&bars[st], (uint32_t)((itp / NS) & 1));  // stage used once per NS iterations
+    if (patch(st, row, x)) __syncthreads();
+    const int fshift = s_fshift[st];
+    T v[E];
+    lds_swz<T, E>(farb(st), fshift + tid * E, v);
+    T gx = v[0], gn = v[0];
+#pragma unroll
+    for (int k = 1; k < E; ++k) {
+      gx = Ord<T>::mx(gx, v[k]);
+      gn = Ord<T>::mn(gn, v[k]);
+    }
+    // last r positions of F_x: [TILE - r, TILE); threads outside borrow the
+    // element at TILE-1, which belongs to every non-empty H range
+    const int hstart = TILE - g.r;
+    T hx, hn;
+    hx = hn = lds_one_swz<T>(farb(st), fshift + TILE - 1);
+    if (tid * E >= hstart) {
+      hx = Ord<T>::mx(hx, gx);
+      hn = Ord<T>::mn(hn, gn);
+    } else if (tid * E + E > hstart) {
+      T vx, vn;
+      suffix_from<T, E>(v, hstart - tid * E, vx, vn);
+      hx = Ord<T>::mx(hx, vx);
+      hn = Ord<T>::mn(hn, vn);
+    }
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+      gx = Ord<T>::mx(gx, __shfl_xor_sync(0xffffffffu, gx, d));
+      gn = Ord<T>::mn(gn, __shfl_xor_sync(0xffffffffu, gn, d));
+      hx = Ord<T>::mx(hx, __shfl_xor_sync(0xffffffffu, hx, d));
+      hn = Ord<T>::mn(hn, __shfl_xor_sync(0xffffffffu, hn, d));
+    }
+    if (lane == 0) {
+      wpub[pb][0][warp] = gx;
+      wpub[pb][1][warp] = gn;
+      wpub[pb][2][warp] = hx;
+      wpub[pb][3][warp] = hn;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const int vv = lane & (NWARP - 1);
+      T a0 = wpub[pb][0][vv], a1 = wpub[pb][1][vv], a2 = wpub[pb][2][vv], a3 = wpub[pb][3][vv];
+#pragma unroll
+      for (int d = NWARP / 2; d >= 1; d >>= 1) {
+        a0 = Ord<T>::mx(a0, __shfl_xor_sync(0xffffffffu, a0, d));
+        a1 = Ord<T>::mn(a1, __shfl_xor_sync(0xffffffffu, a1, d));
+        a2 = Ord<T>::mx(a2, __shfl_xor_sync(0xffffffffu, a2, d));
+        a3 = Ord<T>::mn(a3, __shfl_xor_sync(0xffffffffu, a3, d));
+      }
+      if constexpr (Ws::kPacked) {
+        if (lane < 4) {
+          const T val = lane == 0 ? a0 : lane == 1 ? a1 : lane == 2 ? a2 : a3;
+          st_relaxed_u64(slots + 4 * tk + lane, pack_slot<T>(val));
+        }
+      } else {
+        if (lane == 0) {
+          T *d = reinterpret_cast<T *>(slots + 4 * tk);
+          d[0] = a0;
+          d[1] = a1;
+          d[2] = a2;
+          d[3] = a3;
+          __threadfence();
+          st_release_u32(flags + tk, 1u);
+        }
+      }
+    }
+  };
+
+  // ------------------------------------------------------------- prologue
+  if (tid == 0) {
+    prefetch_tmap(&map);
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    stage_ticket(0);
+    stage_ticket(1);
+  }
+  __syncthreads();
+  publish(0);
+
+  for (int it = 0;; ++it) {
+    const int st = it % NS;
+    const int64_t ticket = s_ticket[st];
+    if (ticket >= g.total) break;
+    // (1) stage ticket it+2 into the stage of ticket it-1 (its readers have all
+    //     passed a barrier since)
+    if (tid == 0) stage_ticket((it + 2) % NS);
+    int64_t row, x;
+    decode(ticket, row, x);
+    const int64_t u0 = x * TILE;
+
+    // look-back loads for this ticket, issued first; thread s covers
+    // x' = x - q + s (H for s == 0 if r > 0, else G)
+    const int64_t lb0 = ticket - g.q;
+    uint64_t pa = 0, pbv = 0;
+    if constexpr (Ws::kPacked) {
+      if (x >= 0 && tid < g.q && !(tid == 0 && g.r == 0)) {
+        const int k = tid == 0 ? 2 : 0;
+        pa = ld_relaxed_u64(slots + 4 * (lb0 + tid) + k);
+        pbv = ld_relaxed_u64(slots + 4 * (lb0 + tid) + k + 1);
+      }
+    }
+
+    // (2) publish ticket it+1 (staged one iteration ago)
+    publish(it + 1);
+
+    // (3) process ticket it: published last iteration, its stage is complete
+    //     and patched
+    if (x < 0) continue;  // publishing-only ticket (uniform)
+    int tout;
+    {
       const int64_t left = p.m - u0;
       tout = left < TILE ? (int)left : TILE;
     }
     const int fshift = s_fshift[st];
-    mbar_wait(&bars[st], (it >> 1) & 1);
-    {  // partial last 128-B row of the series, if staged
-      bool fixed = false;
-      const T *srs = series_ptr<T>(p, row);
-      const int64_t full = p.has_map ? (p.n / RW) * RW : 0;
-      if (full < p.n) {
-        const int64_t fa = f0 - fshift;  // absolute start of the far stage
-        const int64_t fe = f0 + TILE;
-        if (full < fe && p.n > fa) {
-          const int64_t lo = full > fa ? full : fa, hi = p.n < fe ? p.n : fe;
-          for (int64_t i = lo + tid; i < hi; i += NT) sts_swz<T>(farb(st), (int)(i - fa), srs[i]);
-          fixed = true;
-        }
-        if (x >= 0 && full < u0 + TILE && p.n > u0) {
-          const int64_t lo = full > u0 ? full : u0, hi = p.n < u0 + TILE ? p.n : u0 + TILE;
-          for (int64_t i = lo + tid; i < hi; i += NT) sts_swz<T>(nearb(st), (int)(i - u0), srs[i]);
-          fixed = true;
-        }
-      }
-      if (fixed) __syncthreads();
-    }
-
-    // ------------------------------------------- far: CTA prefix scan of F_x
     T ux[E], un[E];  // become max(P, S) per element
-    T hx, hn;
-    {
+    T cx, cn;        // per-thread constant: carries and gap
+    {  // far: prefix scan of F_x
       T v[E];
       lds_swz<T, E>(farb(st), fshift + tid * E, v);
       ux[0] = un[0] = v[0];
@@ -194,133 +311,84 @@ __global__ void __launch_bounds__(NT, 2)
         ux[k] = Ord<T>::mx(ux[k - 1], v[k]);
         un[k] = Ord<T>::mn(un[k - 1], v[k]);
       }
-      // last r positions of F_x: [TILE - r, TILE); lanes outside borrow the
-      // element at TILE-1, which belongs to every non-empty H range
-      const int hstart = TILE - g.r;
-      hx = hn = lds_one_swz<T>(farb(st), fshift + TILE - 1);
-      if (tid * E >= hstart) {
-        hx = Ord<T>::mx(hx, ux[E - 1]);
-        hn = Ord<T>::mn(hn, un[E - 1]);
-      } else if (tid * E + E > hstart) {
-        T vx, vn;
-        suffix_from<T, E>(v, hstart - tid * E, vx, vn);
-        hx = Ord<T>::mx(hx, vx);
-        hn = Ord<T>::mn(hn, vn);
-      }
-    }
-    T ax = ux[E - 1], an = un[E - 1];
+      T ax = ux[E - 1], an = un[E - 1];
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      T vx = shfl_up(ax, d), vn = shfl_up(an, d);
-      if (lane >= d) {
-        ax = Ord<T>::mx(ax, vx);
-        an = Ord<T>::mn(an, vn);
-      }
-    }
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) {  // warp reduce of the H part
-      hx = Ord<T>::mx(hx, __shfl_xor_sync(0xffffffffu, hx, d));
-      hn = Ord<T>::mn(hn, __shfl_xor_sync(0xffffffffu, hn, d));
-    }
-    T cx = shfl_up(ax, 1), cn = shfl_up(an, 1);
-    if (lane == 0) {  // an element inside every window of the chunk
-      cx = ux[0];
-      cn = un[0];
-    }
-    if (lane == 31) {
-      wagg[0][warp] = ax;
-      wagg[1][warp] = an;
-    }
-    if (lane == 0) {
-      wagg[2][warp] = hx;
-      wagg[3][warp] = hn;
-    }
-    __syncthreads();
-    for (int v = 0; v < warp; ++v) {  // cross-warp carry of the prefix
-      cx = Ord<T>::mx(cx, wagg[0][v]);
-      cn = Ord<T>::mn(cn, wagg[1][v]);
-    }
-    // -------------------------------------------------------------- publish
-    if (warp == 0) {
-      T gx = wagg[0][lane & (NWARP - 1)], gn = wagg[1][lane & (NWARP - 1)];
-      T hhx = wagg[2][lane & (NWARP - 1)], hhn = wagg[3][lane & (NWARP - 1)];
-#pragma unroll
-      for (int d = NWARP / 2; d >= 1; d >>= 1) {
-        gx = Ord<T>::mx(gx, __shfl_xor_sync(0xffffffffu, gx, d));
-        gn = Ord<T>::mn(gn, __shfl_xor_sync(0xffffffffu, gn, d));
-        hhx = Ord<T>::mx(hhx, __shfl_xor_sync(0xffffffffu, hhx, d));
-        hhn = Ord<T>::mn(hhn, __shfl_xor_sync(0xffffffffu, hhn, d));
-      }
-      if constexpr (Ws::kPacked) {
-        if (lane < 4) {
-          const T v = lane == 0 ? gx : lane == 1 ? gn : lane == 2 ? hhx : hhn;
-          st_relaxed_u64(slots + 4 * ticket + lane, pack_slot<T>(v));
-        }
-      } else {
-        if (lane == 0) {
-          T *d = reinterpret_cast<T *>(slots + 4 * ticket);
-          d[0] = gx;
-          d[1] = gn;
-          d[2] = hhx;
-          d[3] = hhn;
-          __threadfence();
-          st_release_u32(flags + ticket, 1u);
+      for (int d = 1; d < 32; d <<= 1) {
+        const T vx = shfl_up(ax, d), vn = shfl_up(an, d);
+        if (lane >= d) {
+          ax = Ord<T>::mx(ax, vx);
+          an = Ord<T>::mn(an, vn);
         }
       }
-    }
-    if (x >= 0) {
-      // ------------------------------------------ near: CTA suffix scan of N_x
-      T bx, bn;
-      {
-        T v[E];
-        lds_swz_aligned<T, E>(nearb(st), tid * E, v);
-        T sx = v[E - 1], sn = v[E - 1];
-        ux[E - 1] = Ord<T>::mx(ux[E - 1], sx);
-        un[E - 1] = Ord<T>::mn(un[E - 1], sn);
-#pragma unroll
-        for (int k = E - 2; k >= 0; --k) {
-          sx = Ord<T>::mx(sx, v[k]);
-          sn = Ord<T>::mn(sn, v[k]);
-          ux[k] = Ord<T>::mx(ux[k], sx);
-          un[k] = Ord<T>::mn(un[k], sn);
-        }
-        bx = sx;
-        bn = sn;
-        // suffix carry from later lanes of the warp
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          T dx = shfl_down(bx, d), dn = shfl_down(bn, d);
-          if (lane + d < 32) {
-            bx = Ord<T>::mx(bx, dx);
-            bn = Ord<T>::mn(bn, dn);
-          }
-        }
-        T ex = shfl_down(bx, 1), en = shfl_down(bn, 1);
-        if (lane == 31) {  // an element inside every window of the chunk
-          ex = v[E - 1];
-          en = v[E - 1];
-        }
-        cx = Ord<T>::mx(cx, ex);
-        cn = Ord<T>::mn(cn, en);
+      cx = shfl_up(ax, 1);
+      cn = shfl_up(an, 1);
+      if (lane == 0) {  // an element inside every window of the chunk
+        cx = ux[0];
+        cn = un[0];
       }
-      // --------------------------------- gap M_x from the look-back, in parallel
-      // thread s < q covers x' = x - q + s: H for s == 0 (if r > 0), else G
-      // neutral: the near tile's last element lies inside every window of the tile
-      T mx = lds_one_swz<T>(nearb(st), TILE - 1), mn = mx;
+      if (lane == 31) {
+        wpre[0][warp] = ax;
+        wpre[1][warp] = an;
+      }
+    }
+    T nl;  // the near tile's last element: inside every window of the tile
+    {  // near: suffix scan of N_x, folded into ux/un
+      T v[E];
+      lds_swz_aligned<T, E>(nearb(st), tid * E, v);
+      nl = lds_one_swz<T>(nearb(st), TILE - 1);
+      T sx = v[E - 1], sn = v[E - 1];
+      ux[E - 1] = Ord<T>::mx(ux[E - 1], sx);
+      un[E - 1] = Ord<T>::mn(un[E - 1], sn);
+#pragma unroll
+      for (int k = E - 2; k >= 0; --k) {
+        sx = Ord<T>::mx(sx, v[k]);
+        sn = Ord<T>::mn(sn, v[k]);
+        ux[k] = Ord<T>::mx(ux[k], sx);
+        un[k] = Ord<T>::mn(un[k], sn);
+      }
+      T bx = sx, bn = sn;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const T dx = shfl_down(bx, d), dn = shfl_down(bn, d);
+        if (lane + d < 32) {
+          bx = Ord<T>::mx(bx, dx);
+          bn = Ord<T>::mn(bn, dn);
+        }
+      }
+      T ex = shfl_down(bx, 1), en = shfl_down(bn, 1);
+      if (lane == 31) {  // an element inside every window of the chunk
+        ex = v[E - 1];
+        en = v[E - 1];
+      }
+      cx = Ord<T>::mx(cx, ex);
+      cn = Ord<T>::mn(cn, en);
+      if (lane == 0) {  // lane 0 holds the warp total
+        wsuf[0][warp] = bx;
+        wsuf[1][warp] = bn;
+      }
+    }
+    {  // gap M_x from the look-back
+      T mx = nl, mn = nl;
       for (int s = tid; s < g.q; s += NT) {
         if (s == 0 && g.r == 0) continue;  // H_{x-q} is empty
-        const int64_t src = ticket - g.q + s;
-        const int k = s == 0 ? 2 : 0;  // slot pair: H or G
+        const int k = s == 0 ? 2 : 0;      // slot pair: H or G
+        const int64_t src = lb0 + s;
         T vx, vn;
         if constexpr (Ws::kPacked) {
-          uint64_t a, b;
+          uint64_t a = pa, b = pbv;
+          if (s != tid) {  // q > NT: later rounds load here
+            a = ld_relaxed_u64(slots + 4 * src + k);
+            b = ld_relaxed_u64(slots + 4 * src + k + 1);
+          }
           uint32_t spins = 0;
-          while (((a = ld_relaxed_u64(slots + 4 * src + k)) >> 32) == 0) {
+          while ((a >> 32) == 0) {
             __nanosleep(32);
+            a = ld_relaxed_u64(slots + 4 * src + k);
             if (++spins > (1u << 26)) __trap();  // a lost publish must fail, never hang
           }
-          while (((b = ld_relaxed_u64(slots + 4 * src + k + 1)) >> 32) == 0) {
+          while ((b >> 32) == 0) {
             __nanosleep(32);
+            b = ld_relaxed_u64(slots + 4 * src + k + 1);
             if (++spins > (1u << 26)) __trap();
           }
           vx = unpack_slot<T>(a);
@@ -338,42 +406,42 @@ __global__ void __launch_bounds__(NT, 2)
         mx = Ord<T>::mx(mx, vx);
         mn = Ord<T>::mn(mn, vn);
       }
-      // CTA reduce of the gap, folded into every thread's constant
 #pragma unroll
       for (int d = 16; d >= 1; d >>= 1) {
         mx = Ord<T>::mx(mx, __shfl_xor_sync(0xffffffffu, mx, d));
         mn = Ord<T>::mn(mn, __shfl_xor_sync(0xffffffffu, mn, d));
       }
-      __syncthreads();  // wagg reuse (prefix aggregates consumed above)
       if (lane == 0) {
-        wagg[0][warp] = bx;  // inclusive warp suffix aggregate (lane 0 holds the warp total)
-        wagg[1][warp] = bn;
-        wagg[2][warp] = mx;
-        wagg[3][warp] = mn;
-      }
-      __syncthreads();
-      for (int v = warp + 1; v < NWARP; ++v) {  // cross-warp carry of the suffix
-        cx = Ord<T>::mx(cx, wagg[0][v]);
-        cn = Ord<T>::mn(cn, wagg[1][v]);
-      }
-      if (g.q > 1 || g.r > 0) {
-        for (int v = 0; v < NWARP; ++v) {
-          cx = Ord<T>::mx(cx, wagg[2][v]);
-          cn = Ord<T>::mn(cn, wagg[3][v]);
-        }
-      }
-      const int c0 = tid * E;
-      if (c0 < tout) {
-        T ox[E], on[E];
-#pragma unroll
-        for (int k = 0; k < E; ++k) {
-          ox[k] = Ord<T>::mx(ux[k], cx);
-          on[k] = Ord<T>::mn(un[k], cn);
-        }
-        store_out<T, E>(p, row, u0 + c0, tout - c0, ox, on);
+        wgap[0][warp] = mx;
+        wgap[1][warp] = mn;
       }
     }
-    __syncthreads();  // stage st and wagg are free for the next iteration
+    __syncthreads();  // warp totals of prefix, suffix and gap are in
+    for (int v = 0; v < warp; ++v) {  // cross-warp carry of the far prefix
+      cx = Ord<T>::mx(cx, wpre[0][v]);
+      cn = Ord<T>::mn(cn, wpre[1][v]);
+    }
+    for (int v = warp + 1; v < NWARP; ++v) {  // cross-warp carry of the suffix
+      cx = Ord<T>::mx(cx, wsuf[0][v]);
+      cn = Ord<T>::mn(cn, wsuf[1][v]);
+    }
+#pragma unroll
+    for (int v = 0; v < NWARP; ++v) {
+      cx = Ord<T>::mx(cx, wgap[0][v]);
+      cn = Ord<T>::mn(cn, wgap[1][v]);
+    }
+    const int c0 = tid * E;
+    if (c0 < tout) {
+      T ox[E], on[E];
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        ox[k] = Ord<T>::mx(ux[k], cx);
+        on[k] = Ord<T>::mn(un[k], cn);
+      }
+      store_out<T, E>(p, row, u0 + c0, tout - c0, ox, on);
+    }
+    // wpre/wsuf/wgap are rewritten next iteration only after that iteration's
+    // publish barrier, which every reader here reaches first
   }
 }
 
