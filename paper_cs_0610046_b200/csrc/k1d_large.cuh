@@ -3,6 +3,10 @@
 
 #include "k1d_base.cuh"
 
+#ifndef MM_LARGE_ISSUE
+#define MM_LARGE_ISSUE 1  // 0: lane 0 issues 8-row boxes; 1: lanes issue 32/8-row boxes
+#endif
+
 namespace mm {
 
 // ===================================================================== large
@@ -89,7 +93,7 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
 
 template <typename T>
 __global__ void __launch_bounds__(NT, 2)
-    k1d_large(Rows p, LargeGeom g, void *ws, const __grid_constant__ CUtensorMap map) {
+    k1d_large(Rows p, LargeGeom g, void *ws, const __grid_constant__ TmaMaps maps) {
   using Lay = LargeLayout<T>;
   using Ws = LargeWs<T>;
   constexpr int E = Lay::E;
@@ -122,12 +126,12 @@ __global__ void __launch_bounds__(NT, 2)
     x = tk - row * g.tickets_per_row - g.q;  // may be negative
   };
 
-  // grab a ticket and stage it into stage st (thread 0 only)
-  auto stage_ticket = [&](int st) {
-    const int64_t tk = (int64_t)atomicAdd(counter, 1ull);
-    s_ticket[st] = tk;
+  // stage ticket tk (grabbed an iteration earlier) into stage st: warp 0, the
+  // boxes (32-row "big" ones plus 8-row ones) issued by different lanes
+  auto stage_ticket = [&](int64_t tk, int st) {
+    if (lane == 0) s_ticket[st] = tk;
     if (tk >= g.total) {
-      mbar_arrive_expect_tx(&bars[st], 0);
+      if (lane == 0) mbar_arrive_expect_tx(&bars[st], 0);
       return;
     }
     int64_t row, x;
@@ -135,17 +139,43 @@ __global__ void __launch_bounds__(NT, 2)
     const int64_t u0 = x * TILE;
     const int64_t f0 = u0 + w - 1;
     const int64_t flen = p.n - f0 < TILE ? p.n - f0 : TILE;
-    s_fshift[st] = (int)(f0 - (f0 / RW) * RW);
-    if (p.has_map) {
+    if (lane == 0) s_fshift[st] = (int)(f0 - (f0 / RW) * RW);
+    if (p.has_map && MM_LARGE_ISSUE == 0) {  // lane 0 issues 8-row boxes one by one
+      if (lane == 0) {
+        const int64_t fr0 = f0 / RW, fr1 = (f0 + flen + RW - 1) / RW;
+        const int nfb = (int)((fr1 - fr0 + kBoxRows - 1) / kBoxRows);
+        const int nnb = x >= 0 ? (TILE / RW + kBoxRows - 1) / kBoxRows : 0;
+        mbar_arrive_expect_tx(&bars[st], (uint32_t)(nfb + nnb) * kBoxBytes);
+        for (int k = 0; k < nfb; ++k)
+          tma_box(&maps.small, farb(st) + k * kBoxBytes, (int)(fr0 + k * kBoxRows), (int)row, &bars[st]);
+        for (int k = 0; k < nnb; ++k)
+          tma_box(&maps.small, nearb(st) + k * kBoxBytes, (int)(u0 / RW + k * kBoxRows), (int)row,
+                  &bars[st]);
+      }
+    } else if (p.has_map) {
       const int64_t fr0 = f0 / RW, fr1 = (f0 + flen + RW - 1) / RW;
-      const int nfb = (int)((fr1 - fr0 + kBoxRows - 1) / kBoxRows);
-      const int nnb = x >= 0 ? (TILE / RW + kBoxRows - 1) / kBoxRows : 0;
-      mbar_arrive_expect_tx(&bars[st], (uint32_t)(nfb + nnb) * kBoxBytes);
-      for (int k = 0; k < nfb; ++k)
-        tma_box(&map, farb(st) + k * kBoxBytes, (int)(fr0 + k * kBoxRows), (int)row, &bars[st]);
-      for (int k = 0; k < nnb; ++k)
-        tma_box(&map, nearb(st) + k * kBoxBytes, (int)(u0 / RW + k * kBoxRows), (int)row, &bars[st]);
-    } else {
+      const int frows = (int)(fr1 - fr0);
+      const int nrows = x >= 0 ? TILE / RW : 0;
+      const int fbig = frows / kBigRows, fsm = (frows - fbig * kBigRows + kBoxRows - 1) / kBoxRows;
+      const int nbig = nrows / kBigRows, nsm = (nrows - nbig * kBigRows + kBoxRows - 1) / kBoxRows;
+      if (lane == 0)
+        mbar_arrive_expect_tx(&bars[st], (uint32_t)((fbig + nbig) * kBigBytes + (fsm + nsm) * kBoxBytes));
+      __syncwarp();
+      const int nf = fbig + fsm, ntot = nf + nbig + nsm;
+      for (int k = lane; k < ntot; k += 32) {
+        if (k < fbig)
+          tma_box(&maps.big, farb(st) + k * kBigBytes, (int)(fr0 + k * kBigRows), (int)row, &bars[st]);
+        else if (k < nf)
+          tma_box(&maps.small, farb(st) + fbig * kBigBytes + (k - fbig) * kBoxBytes,
+                  (int)(fr0 + fbig * kBigRows + (k - fbig) * kBoxRows), (int)row, &bars[st]);
+        else if (k < nf + nbig)
+          tma_box(&maps.big, nearb(st) + (k - nf) * kBigBytes, (int)(u0 / RW + (k - nf) * kBigRows),
+                  (int)row, &bars[st]);
+        else
+          tma_box(&maps.small, nearb(st) + nbig * kBigBytes + (k - nf - nbig) * kBoxBytes,
+                  (int)(u0 / RW + nbig * kBigRows + (k - nf - nbig) * kBoxRows), (int)row, &bars[st]);
+      }
+    } else if (lane == 0) {
       mbar_arrive_expect_tx(&bars[st], 0);
     }
   };
@@ -255,12 +285,24 @@ __global__ void __launch_bounds__(NT, 2)
   };
 
   // ------------------------------------------------------------- prologue
+  // warp 0 holds the next ticket number in a register, grabbed one iteration
+  // before it is staged (the atomic's latency never sits on the critical path)
+  unsigned long long tk_next = 0;
   if (tid == 0) {
-    prefetch_tmap(&map);
+    prefetch_tmap(&maps.big);
+    prefetch_tmap(&maps.small);
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
-    stage_ticket(0);
-    stage_ticket(1);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long t0 = 0, t1 = 0;
+    if (lane == 0) {
+      t0 = atomicAdd(counter, 1ull);
+      t1 = atomicAdd(counter, 1ull);
+    }
+    stage_ticket((int64_t)__shfl_sync(0xffffffffu, t0, 0), 0);
+    stage_ticket((int64_t)__shfl_sync(0xffffffffu, t1, 0), 1);
   }
   __syncthreads();
   publish(0);
@@ -270,8 +312,11 @@ __global__ void __launch_bounds__(NT, 2)
     const int64_t ticket = s_ticket[st];
     if (ticket >= g.total) break;
     // (1) stage ticket it+2 into the stage of ticket it-1 (its readers have all
-    //     passed a barrier since)
-    if (tid == 0) stage_ticket((it + 2) % NS);
+    //     passed a barrier since), and grab ticket it+3
+    if (warp == 0) {
+      if (lane == 0) tk_next = atomicAdd(counter, 1ull);
+      stage_ticket((int64_t)__shfl_sync(0xffffffffu, tk_next, 0), (it + 2) % NS);
+    }
     int64_t row, x;
     decode(ticket, row, x);
     const int64_t u0 = x * TILE;

@@ -22,7 +22,7 @@ enum : int { kOK = 0, kErrWorkspace = 8, kErrCuda = 9, kErrUnsupported = 10 };
 int note_cuda(cudaError_t e);  // records the error (thread-local), returns kErrCuda or kOK
 int sm_count();                // SMs of the current device (cached)
 int encode_rows_map(CUtensorMap *map, const void *in, int elem_bytes, int64_t rows_per_series,
-                    int64_t batch, int64_t in_ld_bytes);  // maxmin_abi.cu
+                    int64_t batch, int64_t in_ld_bytes, int box_rows = kBoxRows);  // maxmin_abi.cu
 
 // Tile geometry of the 1-D kernels for element type T.
 template <typename T>
@@ -168,8 +168,16 @@ static int launch_medium(const Rows &p, const CUtensorMap &map, cudaStream_t s) 
 }
 
 template <typename T>
-static int launch_large(const Rows &p, const CUtensorMap &map, void *ws, size_t ws_bytes,
+static int launch_large(const Rows &p, const CUtensorMap &small, void *ws, size_t ws_bytes,
                         cudaStream_t s) {
+  TmaMaps map;
+  map.small = small;
+  std::memset(&map.big, 0, sizeof(map.big));
+  if (p.has_map) {
+    int rc = encode_rows_map(&map.big, p.in, (int)sizeof(T), p.n / Rowing<T>::RW, p.batch,
+                             p.in_ld * (int64_t)sizeof(T), kBigRows);
+    if (rc) return rc;
+  }
   constexpr int64_t TILE = Geo1D<T>::TILE;
   LargeGeom g;
   g.q = (int)((p.w - 1) / TILE);

@@ -49,7 +49,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // 3-D map {RW, rows_per_series, batch} of 128-byte rows, boxes {RW, 8, 1},
 // 128-byte swizzle, zero fill out of bounds (tma.cuh).
 int encode_rows_map(CUtensorMap *map, const void *in, int elem_bytes, int64_t rows_per_series,
-                    int64_t batch, int64_t in_ld_bytes) {
+                    int64_t batch, int64_t in_ld_bytes, int box_rows) {
   auto fn = encode_fn();
   if (!fn) return note_cuda(cudaErrorNotSupported);
   CUtensorMapDataType dt = elem_bytes == 1   ? CU_TENSOR_MAP_DATA_TYPE_UINT8
@@ -59,7 +59,7 @@ int encode_rows_map(CUtensorMap *map, const void *in, int elem_bytes, int64_t ro
   const cuuint64_t RW = 128 / elem_bytes;
   cuuint64_t dims[3] = {RW, (cuuint64_t)rows_per_series, (cuuint64_t)batch};
   cuuint64_t strides[2] = {128, (cuuint64_t)(batch > 1 ? in_ld_bytes : rows_per_series * 128)};
-  cuuint32_t box[3] = {(cuuint32_t)RW, (cuuint32_t)kBoxRows, 1};
+  cuuint32_t box[3] = {(cuuint32_t)RW, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, dt, 3, const_cast<void *>(in), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

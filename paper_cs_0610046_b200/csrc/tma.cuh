@@ -114,6 +114,15 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
+// Two maps over the same rows (k1d_large): boxes of 32 rows (4 KB) and of 8
+// rows (1 KB); a staged range is covered by big boxes plus a few small ones.
+constexpr int kBigRows = 32;
+constexpr int kBigBytes = 128 * kBigRows;
+struct TmaMaps {
+  CUtensorMap big;
+  CUtensorMap small;
+};
+
 // Stage logical elements [e0, e0+len) of series b (e0 % RW arbitrary) into buf
 // starting at buf row 0 = series row floor(e0/RW).  Issues whole boxes and arms
 // the barrier.  Returns the logical offset of e0 inside buf.
