@@ -241,7 +241,7 @@ def run_1d(args, rank, world, local):
     windows = cfg["windows"]
     n_local = cfg["n"]
     wmax = max(windows)
-    halo = (wmax - 1) if world > 1 and rank < world - 1 else 0
+    halo = (wmax - 1) if world > 1 else 0
     chunk = shard.Chunk1D(rank=rank, world=world, n_local=n_local, halo=halo)
     dev = torch.device("cuda", local)
 

@@ -1,0 +1,166 @@
+"""bench.py --config C1|C3|C4: the other BASELINE.json workloads (item-sharded,
+no communication).  Same JSON line schema as bench.py; imported by bench.py."""
+from __future__ import annotations
+
+import json
+import os
+import time
+
+import bench
+
+
+def _timed(step, steps, warmup, world, dev):
+    import torch
+    import torch.distributed as dist
+
+    for _ in range(warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with bench.ClockSampler(torch.cuda.current_device()) as clk:
+        e0.record(s)
+        for _ in range(steps):
+            step()
+        e1.record(s)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()), clk.summary()
+
+
+def run_extra(args, rank, world, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_cs_0610046_b200 as mm
+    from paper_cs_0610046_b200 import shard
+    import synth
+
+    dev = torch.device("cuda", local)
+    peak, peak_src = bench.load_peaks()
+    cfg = args.config
+    if cfg == "C1":
+        n, w = synth.C1["n"], synth.C1["w"]
+        host = synth.c1()
+        x = torch.from_numpy(host).to(dev)
+        ox = torch.empty(n - w + 1, dtype=torch.float64, device=dev)
+        on = torch.empty_like(ox)
+
+        def step():
+            mm.maxmin_filter_1d(x, w, out_max=ox, out_min=on)
+
+        nb = 8 * (n + 2 * (n - w + 1))
+        outs = 2 * (n - w + 1) * world
+        steps = max(args.steps, 200)
+        name = "C1: 1-D fp64 U[0,1) n=100000, w=16 (launch/L2-bound: 2.4 MB per call)"
+        dtype = "f64"
+        l2 = "2.4 MB working set stays in L2 (not a roofline point, launch-bound)"
+        ex, en, _ = __import__("oracle").brute_1d(host, w)
+        mm.maxmin_filter_1d(x, w, out_max=ox, out_min=on)
+        parity = bool(np.array_equal(ox.cpu().numpy(), ex) and np.array_equal(on.cpu().numpy(), en))
+        ms, clk = _timed(step, steps, args.warmup, world, dev)
+        sample = host
+        windows = (w,)
+    elif cfg == "C3":
+        B, n, w = synth.C3["batch"], synth.C3["n"], synth.C3["w"]
+        r0, r1 = shard.shard_items(B, world, rank)
+        rows = r1 - r0
+        host = torch.empty(rows, n, dtype=torch.float32).pin_memory()
+        synth.c3(rows=rows, row0=r0, out=host.numpy())
+        x = host.to(dev)
+        m = n - w + 1
+        ox = torch.empty(rows, m, dtype=torch.float32, device=dev)
+        on = torch.empty_like(ox)
+
+        def step():
+            mm.maxmin_filter_batched(x, w, out_max=ox, out_min=on)
+
+        nb = 4 * rows * (n + 2 * m)
+        outs = 2 * m * B
+        steps = args.steps
+        name = "C3: 65536 fp32 series x 4096 (sine + N(0,0.1) noise), w=129, sharded by series"
+        dtype = "f32"
+        l2 = "inputs (1 GiB) larger than the 126 MB L2"
+        step()
+        torch.cuda.synchronize()
+        import oracle
+
+        k = min(rows, 512)
+        ex, en = oracle.batched(host[:k].numpy(), w)
+        parity = bool(np.array_equal(ox[:k].cpu().numpy(), ex) and np.array_equal(on[:k].cpu().numpy(), en))
+        ms, clk = _timed(step, steps, args.warmup, world, dev)
+        sample = host[:2048].numpy()
+        windows = (w,)
+    elif cfg == "C4":
+        NI, R, C, w = synth.C4["batch"], synth.C4["rows"], synth.C4["cols"], synth.C4["w_row"]
+        i0, i1 = shard.shard_items(NI, world, rank)
+        cnt = i1 - i0
+        host = torch.empty(cnt, R, C, dtype=torch.uint8).pin_memory()
+        synth.c4(count=cnt, img0=i0, out=host.numpy())
+        x = host.to(dev)
+        Ro, Co = R - w + 1, C - w + 1
+        ox = torch.empty(cnt, Ro, C, dtype=torch.uint8, device=dev)  # out_ld = cols (16-B rows)
+        on = torch.empty_like(ox)
+
+        def step():
+            mm.maxmin_filter_2d(x, w, w, out_max=ox[:, :, :Co], out_min=on[:, :, :Co])
+
+        nb = cnt * (R * C + 2 * Ro * Co)
+        outs = 2 * Ro * Co * NI
+        steps = max(1, args.steps // 5)
+        name = "C4: 8 uint8 images 16384x16384 (iid + 64 rectangles), 2-D w=15x15, sharded by image"
+        dtype = "u8"
+        l2 = "inputs (2 GiB) larger than the 126 MB L2"
+        step()
+        torch.cuda.synchronize()
+        import oracle
+
+        crop = host[0, :300, :400].numpy().copy()
+        cx, cn = oracle.separable_2d(crop, w, w)
+        parity = bool(np.array_equal(ox[0, :300 - w + 1, :400 - w + 1].cpu().numpy(), cx)
+                      and np.array_equal(on[0, :300 - w + 1, :400 - w + 1].cpu().numpy(), cn))
+        ms, clk = _timed(step, steps, args.warmup, world, dev)
+        sample = None
+        windows = (w,)
+    else:
+        raise SystemExit(f"unknown config {cfg}")
+
+    ms_step = ms / steps
+    value = outs / (ms_step / 1e3)
+    achieved = nb / (ms_step / 1e3) / 1e9
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu and world == 1 and sample is not None:
+            cpu = bench.cpu_baseline(cfg, np.ascontiguousarray(sample).reshape(-1) if cfg != "C3" else sample,
+                                     windows, None) if cfg == "C1" else _cpu_batched(sample, windows[0])
+        line = {
+            "metric": bench.METRIC, "value": value, "unit": bench.UNIT, "n_gpus": world, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": {"workload": name, "l2": l2,
+                       "parallelism": f"item sharding, dp{world}" if world > 1 else "single GPU"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src},
+            "cpu_baseline": cpu, "e2e": None, "gpu_launches": steps, "clocks": clk,
+            "parity": {"bit_exact": parity},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _cpu_batched(sample, w):
+    import oracle
+
+    t0 = time.perf_counter()
+    mx, mn = oracle.batched(sample, w)
+    dt = time.perf_counter() - t0
+    return {"value": 2 * mx.size / dt, "unit": bench.UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{sample.shape[0]} series x {sample.shape[1]}, oracle_batched (appendix per row), {dt:.2f} s"}

@@ -25,7 +25,7 @@ class Chunk1D:
     rank: int
     world: int
     n_local: int  # elements this rank owns
-    halo: int     # w_max - 1 elements received from rank+1 (0 on the last rank)
+    halo: int     # w_max - 1: elements sent to rank-1 and received from rank+1
 
     @property
     def last(self) -> bool:
