@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmaxmin.so")
+# MAXMIN_LIB selects another in-tree build (A/B experiments); default libmaxmin.so
+LIB_PATH = os.path.join(_HERE, os.environ.get("MAXMIN_LIB", "libmaxmin.so"))
 
 # maxmin_dtype (include/maxmin.h)
 U8, I8, U16, I16, U32, I32, U64, I64, F32, F64 = range(10)

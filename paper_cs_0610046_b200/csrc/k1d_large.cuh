@@ -3,6 +3,12 @@
 
 #include "k1d_base.cuh"
 
+#ifndef MM_STAGE_POS
+#define MM_STAGE_POS 1  // 0: stage before the publish step, 1: right after it
+#endif
+#ifndef MM_STAGE_WARP
+#define MM_STAGE_WARP 7  // the warp that grabs and stages tickets (not warp 0, which publishes)
+#endif
 #ifndef MM_LARGE_ISSUE
 #define MM_LARGE_ISSUE 1  // 0: lane 0 issues 8-row boxes; 1: lanes issue 32/8-row boxes
 #endif
@@ -313,7 +319,7 @@ __global__ void __launch_bounds__(NT, 2)
     if (ticket >= g.total) break;
     // (1) stage ticket it+2 into the stage of ticket it-1 (its readers have all
     //     passed a barrier since), and grab ticket it+3
-    if (warp == 0) {
+    if (MM_STAGE_POS == 0 && warp == MM_STAGE_WARP) {
       if (lane == 0) tk_next = atomicAdd(counter, 1ull);
       stage_ticket((int64_t)__shfl_sync(0xffffffffu, tk_next, 0), (it + 2) % NS);
     }
@@ -335,6 +341,10 @@ __global__ void __launch_bounds__(NT, 2)
 
     // (2) publish ticket it+1 (staged one iteration ago)
     publish(it + 1);
+    if (MM_STAGE_POS == 1 && warp == MM_STAGE_WARP) {
+      if (lane == 0) tk_next = atomicAdd(counter, 1ull);
+      stage_ticket((int64_t)__shfl_sync(0xffffffffu, tk_next, 0), (it + 2) % NS);
+    }
 
     // (3) process ticket it: published last iteration, its stage is complete
     //     and patched
