@@ -348,7 +348,13 @@ __global__ void __launch_bounds__(NT, 2)
 
     // (3) process ticket it: published last iteration, its stage is complete
     //     and patched
-    if (x < 0) continue;  // publishing-only ticket (uniform)
+    if (x < 0) {  // publishing-only ticket (uniform)
+      // the stage warp wrote s_ticket/s_fshift of ticket it+2 after publish(it+1)'s
+      // barrier; publish(it+2) reads them next iteration, so order the write
+      // here just as the process step's barrier does for x >= 0
+      __syncthreads();
+      continue;
+    }
     int tout;
     {
       const int64_t left = p.m - u0;

@@ -117,6 +117,24 @@ def test_batched_rows(cuda_device, w):
     assert_same(mn, en, f"batched min w={w}")
 
 
+@pytest.mark.parametrize("dtype", [np.uint8, np.int8, np.float32, np.float64],
+                         ids=lambda d: np.dtype(d).name)
+def test_large_window_repeated(cuda_device, dtype):
+    """The look-back kernel's ticket ring, many rows and many launches: each row
+    starts with q publishing-only tickets, so ordering bugs between the stage
+    warp and the publish step show up as sporadic mismatches or faults."""
+    rows, n = 24, 40_000
+    a = synth.random_values(dtype, rows * n, seed=4242).reshape(rows, n)
+    x = torch.from_numpy(a).to(dev())
+    for w in (8194, 10_000, 17_000, 39_999):
+        ex, en = oracle.batched(a, w)
+        for _ in range(10):
+            mx, mn = mm.maxmin_filter_batched(x, w)
+            torch.cuda.synchronize()
+            assert_same(mx, ex, f"max w={w}")
+            assert_same(mn, en, f"min w={w}")
+
+
 def test_c3_shape_sample(cuda_device):
     """C3 layout [65536][4096] f32, w=129; parity on a 2048-row slice (full size in bench)."""
     rows = 2048
