@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(NT2) k2d_generic(Img2D p) {
   const int wr = p.w_row, wc = p.w_col;
   const int P = Tl::pitch(wr);
   const int BH = TH + wc - 1;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   T *Ax = reinterpret_cast<T *>(smem_raw);  // ping (max)
   T *An = Ax + (size_t)BH * P;                // ping (min)
   T *Bx = An + (size_t)BH * P;                // pong (max)

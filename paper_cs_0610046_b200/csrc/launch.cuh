@@ -10,6 +10,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstring>
+#include <type_traits>
 
 #include "k1d.cuh"
 #include "k2d.cuh"
@@ -21,6 +22,12 @@ enum : int { kOK = 0, kErrWorkspace = 8, kErrCuda = 9, kErrUnsupported = 10 };
 
 int note_cuda(cudaError_t e);  // records the error (thread-local), returns kErrCuda or kOK
 int sm_count();                // SMs of the current device (cached)
+// packed 1-byte 2-D kernel (k2d_byte.cu); kErrUnsupported when it does not apply
+int launch_2d_byte(bool is_signed, const void *in, int64_t batch, int64_t rows, int64_t cols,
+                   int64_t in_ld, int64_t in_bstride, int64_t w_row, int64_t w_col, void *out_max,
+                   void *out_min, int64_t out_ld, int64_t out_bstride, cudaStream_t s);
+int encode_u8_map(CUtensorMap *map, const void *base, const int64_t dims[3], const int64_t strides[2],
+                  const int box[3]);  // maxmin_abi.cu
 int encode_rows_map(CUtensorMap *map, const void *in, int elem_bytes, int64_t rows_per_series,
                     int64_t batch, int64_t in_ld_bytes, int box_rows = kBoxRows);  // maxmin_abi.cu
 
@@ -255,6 +262,11 @@ int launch_2d(const void *in, int64_t batch, int64_t rows, int64_t cols, int64_t
               int64_t in_bstride, int64_t w_row, int64_t w_col, void *out_max, void *out_min,
               int64_t out_ld, int64_t out_bstride, cudaStream_t s) {
   if (batch == 0) return kOK;
+  if constexpr (sizeof(T) == 1) {
+    const int rc = launch_2d_byte(std::is_signed<T>::value, in, batch, rows, cols, in_ld, in_bstride,
+                                  w_row, w_col, out_max, out_min, out_ld, out_bstride, s);
+    if (rc != kErrUnsupported) return rc;
+  }
   const size_t smem = smem_2d<T>(w_row, w_col);
   if (smem > 200 * 1024) return kErrUnsupported;
   auto kern = k2d_generic<T>;

@@ -68,6 +68,24 @@ int encode_rows_map(CUtensorMap *map, const void *in, int elem_bytes, int64_t ro
   return kOK;
 }
 
+// Generic 3-D byte-element tiled map (no swizzle, zero fill): dims {d0, d1, d2},
+// byte strides {s1, s2} of dims 1 and 2, box {b0, b1, b2}.  Used by the packed
+// 1-byte 2-D kernel for its input stages and its output stores (k2d_byte.cu).
+int encode_u8_map(CUtensorMap *map, const void *base, const int64_t dims[3], const int64_t strides[2],
+                  const int box[3]) {
+  auto fn = encode_fn();
+  if (!fn) return note_cuda(cudaErrorNotSupported);
+  cuuint64_t d[3] = {(cuuint64_t)dims[0], (cuuint64_t)dims[1], (cuuint64_t)dims[2]};
+  cuuint64_t st[2] = {(cuuint64_t)strides[0], (cuuint64_t)strides[1]};
+  cuuint32_t bx[3] = {(cuuint32_t)box[0], (cuuint32_t)box[1], (cuuint32_t)box[2]};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void *>(base), d, st, bx, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return note_cuda(cudaErrorInvalidValue);
+  return kOK;
+}
+
 MM_DECLARE_INST(uint8_t)
 MM_DECLARE_INST(int8_t)
 MM_DECLARE_INST(uint16_t)

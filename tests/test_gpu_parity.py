@@ -279,3 +279,53 @@ def test_device_errors(cuda_device):
     out = torch.empty(998, device=dev())
     rc = L.maxmin_filter_1d(8, host.data_ptr(), 1000, 3, out.data_ptr(), None, None, 0, None)
     assert rc == 11  # host pointer passed to the device API
+
+
+# ------------------------------------------------- packed 1-byte 2-D path ---
+# k2d_byte takes square windows 2..17 when rows/pitches are 16-B multiples;
+# shapes below span several 1024-column strips, ragged right edges, short
+# images and CTA row ranges that straddle images.
+BYTE_W = [2, 3, 4, 5, 7, 9, 11, 13, 15, 16, 17]
+
+
+@pytest.mark.parametrize("w", BYTE_W)
+@pytest.mark.parametrize("dtype", [np.uint8, np.int8], ids=lambda d: np.dtype(d).name)
+def test_2d_byte_fast_path(cuda_device, w, dtype):
+    img = synth.c4(count=3, rows=203, cols=2096, nrect=12)
+    if dtype == np.int8:
+        img = img.view(np.int8)
+    x = torch.from_numpy(img).to(dev())
+    mx, mn = mm.maxmin_filter_2d(x, w, w)
+    ex, en = oracle.separable_2d(img, w, w)
+    assert_same(mx, ex, f"2d max {w}x{w}")
+    assert_same(mn, en, f"2d min {w}x{w}")
+
+
+@pytest.mark.parametrize("shape", [(1, 15, 16), (2, 15, 1040), (5, 40, 1024), (1, 700, 3088),
+                                   (9, 17, 1056), (2, 1000, 48)])
+def test_2d_byte_shapes(cuda_device, shape):
+    b, r, c = shape
+    img = synth.c4(count=b, rows=r, cols=c, nrect=4)
+    x = torch.from_numpy(img).to(dev())
+    for w in (15, 3):
+        if w > r:
+            continue
+        mx, mn = mm.maxmin_filter_2d(x, w, w)
+        ex, en = oracle.separable_2d(img, w, w)
+        assert_same(mx, ex, f"2d max {shape} w={w}")
+        assert_same(mn, en, f"2d min {shape} w={w}")
+
+
+def test_2d_byte_strided_single_output(cuda_device):
+    """C4 output convention (out_ld = cols, 16-B rows) and one output only."""
+    img = synth.c4(count=2, rows=300, cols=2048, nrect=6)
+    x = torch.from_numpy(img).to(dev())
+    R, C = 300 - 14, 2048 - 14
+    ox = torch.zeros(2, R, 2048, dtype=torch.uint8, device=dev())
+    on = torch.zeros(2, R, 2048, dtype=torch.uint8, device=dev())
+    ex, en = oracle.separable_2d(img, 15, 15)
+    mm.maxmin_filter_2d(x, 15, 15, out_max=ox[:, :, :C], want_min=False)
+    mm.maxmin_filter_2d(x, 15, 15, out_min=on[:, :, :C], want_max=False)
+    assert_same(ox[:, :, :C].contiguous(), ex)
+    assert_same(on[:, :, :C].contiguous(), en)
+    assert int(ox[:, :, C:].sum()) == 0 and int(on[:, :, C:].sum()) == 0
