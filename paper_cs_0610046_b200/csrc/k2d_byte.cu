@@ -1,16 +1,16 @@
 // k2d_byte.cu -- instantiation and launcher of the packed 1-byte 2-D kernel
-// (k2d_byte.cuh).  Square windows 2..17 are compiled in; other shapes, other
-// element types and layouts the kernel does not take (16-B aligned rows and
-// pitches for the bulk copies in and out) go to
-// k2d_generic.
+// (k2d_byte.cuh).  Square windows 2..17 are compiled in.  Other shapes, other
+// element types and layouts the kernel does not take (the input's rows and
+// pitches 16-B aligned for TMA, output rows 4-B aligned for the word stores)
+// go to k2d_generic.
 #include "launch.cuh"
 #include "k2d_byte.cuh"
 
 namespace mm {
 
 template <bool SG, int WR, int WC>
-static int launch_byte(const k2b::Args &a, const k2b::Maps &maps, cudaStream_t s) {
-  constexpr size_t smem = k2b::Smem<WR>::BYTES;
+static int launch_byte(const k2b::Args &a, const CUtensorMap &map, cudaStream_t s) {
+  constexpr size_t smem = k2b::Smem::BYTES;
   auto kern = k2b::k2d_byte<SG, WR, WC>;
   static size_t attr = 0;
   int rc = set_smem(kern, smem, attr);
@@ -20,15 +20,13 @@ static int launch_byte(const k2b::Args &a, const k2b::Maps &maps, cudaStream_t s
   if (e != cudaSuccess) return note_cuda(e);
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)per_sm * sm_count();
-  // at least ~RB output rows per CTA, so tiny images do not spread thin
-  const int64_t cap = (a.units + k2b::RB - 1) / k2b::RB;
-  if (grid > cap) grid = cap > 0 ? cap : 1;
-  kern<<<(unsigned)grid, k2b::NTB, smem, s>>>(a, maps);
+  if (grid > a.ntiles) grid = a.ntiles;
+  kern<<<(unsigned)grid, k2b::NTB, smem, s>>>(a, map);
   return note_cuda(cudaGetLastError());
 }
 
 template <bool SG>
-static int dispatch_square(const k2b::Args &a, const k2b::Maps &m, int w, cudaStream_t s) {
+static int dispatch_square(const k2b::Args &a, const CUtensorMap &m, int w, cudaStream_t s) {
   switch (w) {
     case 2: return launch_byte<SG, 2, 2>(a, m, s);
     case 3: return launch_byte<SG, 3, 3>(a, m, s);
@@ -50,44 +48,40 @@ int launch_2d_byte(bool is_signed, const void *in, int64_t batch, int64_t rows, 
                    void *out_min, int64_t out_ld, int64_t out_bstride, cudaStream_t s) {
   if (w_row != w_col || w_row > k2b::MAXW) return kErrUnsupported;
   auto al = [](const void *p, uintptr_t m) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) % m) == 0; };
-  if (!al(in, 16) || in_ld % 16 || cols % 16 || (batch > 1 && in_bstride % 16)) return kErrUnsupported;
-  if (!al(out_max, 16) || !al(out_min, 16) || out_ld % 16 || (batch > 1 && out_bstride % 16))
+  if (!al(in, 16) || in_ld % 16 || (batch > 1 && in_bstride % 16)) return kErrUnsupported;
+  if (!al(out_max, 4) || !al(out_min, 4) || out_ld % 4 || (batch > 1 && out_bstride % 4))
+    return kErrUnsupported;
+  if (cols > 0x7fffffffLL || rows > 0x7fffffffLL || batch > 0x7fffffffLL || out_ld > (0xffffffffLL / k2b::RB))
     return kErrUnsupported;
   k2b::Args a;
-  a.in = static_cast<const uint8_t *>(in);
   a.out_max = static_cast<uint8_t *>(out_max);
   a.out_min = static_cast<uint8_t *>(out_min);
   a.batch = batch;
   a.rows = rows;
   a.cols = cols;
-  a.in_ld = in_ld;
-  a.in_bstride = batch > 1 ? in_bstride : 0;
   a.out_ld = out_ld;
   a.out_bstride = batch > 1 ? out_bstride : 0;
   a.Ro = rows - w_col + 1;
   a.Co = cols - w_row + 1;
-  a.Co16 = a.Co & ~int64_t(15);
   a.nstrip = (a.Co + k2b::TW - 1) / k2b::TW;
-  a.units = batch * a.nstrip * a.Ro;
-  if (a.units == 0) return kOK;
-  if (cols > 0x7fffffffLL || rows > 0x7fffffffLL || batch > 0x7fffffffLL) return kErrUnsupported;
-  // TMA maps: input {cols, rows, batch} in 256- and 16-column boxes of RB rows;
-  // outputs {Co, Ro, batch} in 256 x RB and 256 x 1 boxes (the 1-row boxes store
-  // the partial stages at the ends of a CTA's row range)
-  k2b::Maps m;
+  // bands of BH output rows: BH + w_col - 1 input rows is a whole number of
+  // RB-row stages, so only an image's last band has a partial stage
+  a.BH = 32 * k2b::RB - (w_col - 1);
+  a.nbands = (a.Ro + a.BH - 1) / a.BH;
+  a.ntiles = batch * a.nbands * a.nstrip;
+  a.one = 1u;
+  a.k8 = 1u << 8;
+  a.k16 = 1u << 16;
+  a.k24 = 1u << 24;
+  if (a.ntiles == 0) return kOK;
+  // TMA map over the input {cols, rows, batch}, boxes {176, RB, 1}; columns
+  // past the image (the last strip's halo) read as zeros and are never output
+  CUtensorMap m;
   std::memset(&m, 0, sizeof(m));
   const int64_t idims[3] = {cols, rows, batch};
   const int64_t istr[2] = {in_ld, batch > 1 ? in_bstride : rows * in_ld};
-  const int bin[3] = {k2b::BOXW, k2b::RB, 1}, btail[3] = {k2b::TAILW, k2b::RB, 1};
-  int rc = encode_u8_map(&m.in_box, in, idims, istr, bin);
-  if (!rc) rc = encode_u8_map(&m.in_tail, in, idims, istr, btail);
-  const int64_t odims[3] = {a.Co16 > 0 ? a.Co16 : 16, a.Ro, batch};  // unused when Co16 == 0
-  const int64_t ostr[2] = {out_ld, batch > 1 ? out_bstride : a.Ro * out_ld};
-  const int bo[3] = {k2b::BOXW, k2b::RB, 1}, bo1[3] = {k2b::BOXW, 1, 1};
-  if (!rc && out_max) rc = encode_u8_map(&m.omx, out_max, odims, ostr, bo);
-  if (!rc && out_max) rc = encode_u8_map(&m.omx1, out_max, odims, ostr, bo1);
-  if (!rc && out_min) rc = encode_u8_map(&m.omn, out_min, odims, ostr, bo);
-  if (!rc && out_min) rc = encode_u8_map(&m.omn1, out_min, odims, ostr, bo1);
+  const int box[3] = {k2b::BOXW, k2b::RB, 1};
+  const int rc = encode_u8_map(&m, in, idims, istr, box);
   if (rc) return rc;
   return is_signed ? dispatch_square<true>(a, m, (int)w_row, s) : dispatch_square<false>(a, m, (int)w_row, s);
 }
