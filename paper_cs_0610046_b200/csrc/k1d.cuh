@@ -7,3 +7,4 @@
 #include "k1d_small.cuh"
 #include "k1d_medium.cuh"
 #include "k1d_large.cuh"
+#include "k1d_warp.cuh"

@@ -38,19 +38,47 @@ struct Geo1D {
   static constexpr int TILE = NT * E;
 };
 
-enum class Path1D { Copy, Small, Medium, Large };
+enum class Path1D { Copy, Small, Medium, Large, Warp };
+
+#ifndef MM_WARP_MIN_W  // smallest window routed to k1d_warp (<= 4-byte types): it
+#define MM_WARP_MIN_W (kHaloMax + 2)  // beats k1d_large, not (yet) k1d_medium
+#endif
 
 template <typename T>
 Path1D path_1d(int64_t w) {
   if (w == 1) return Path1D::Copy;
   if (w <= Geo1D<T>::E) return Path1D::Small;
+  if constexpr (sizeof(T) <= 4) {
+    if (w - 1 >= WarpGeo<T>::WT && w >= MM_WARP_MIN_W) return Path1D::Warp;
+  }
   if (w - 1 <= kHaloMax) return Path1D::Medium;
   return Path1D::Large;
 }
 
 template <typename T>
+WarpLB warp_geom(int64_t batch, int64_t n, int64_t w) {
+  WarpLB g{};
+  if constexpr (sizeof(T) <= 4) {
+    constexpr int64_t WT = WarpGeo<T>::WT, K = WarpGeo<T>::K;
+    const int64_t m = n - w + 1;
+    g.q = (int)((w - 1) / WT);
+    g.r = (int)((w - 1) % WT);
+    g.tpr = (m + WT - 1) / WT;
+    g.xr = g.q + g.tpr;
+    g.kt = (g.xr + K - 1) / K;
+    g.total = batch * g.kt;
+    g.pg = (int)((g.q + K - 1) / K + 1);
+  }
+  return g;
+}
+
+template <typename T>
 size_t workspace_1d(int64_t batch, int64_t n, int64_t w) {
-  if (path_1d<T>(w) != Path1D::Large || batch == 0) return 0;
+  if (batch == 0) return 0;
+  if constexpr (sizeof(T) <= 4) {
+    if (path_1d<T>(w) == Path1D::Warp) return WarpWs<T>::bytes(warp_geom<T>(batch, n, w), batch);
+  }
+  if (path_1d<T>(w) != Path1D::Large) return 0;
   const int64_t TILE = Geo1D<T>::TILE;
   const int64_t m = n - w + 1;
   const int64_t tpr = (m + TILE - 1) / TILE;
@@ -207,6 +235,51 @@ static int launch_large(const Rows &p, const CUtensorMap &small, void *ws, size_
   return note_cuda(cudaGetLastError());
 }
 
+template <typename T>
+static int launch_warp(const Rows &p, void *ws, size_t ws_bytes, cudaStream_t s) {
+  if constexpr (sizeof(T) > 4) {
+    return kErrUnsupported;
+  } else {
+    using Geo = WarpGeo<T>;
+    // maps over the whole 128-B rows: near chunks {RW, 16} and far chunks {RW, 17}
+    TmaMaps map;
+    std::memset(&map, 0, sizeof(map));
+    const int64_t full_rows = p.n / Rowing<T>::RW;
+    int rc = encode_rows_map(&map.big, p.in, (int)sizeof(T), full_rows, p.batch,
+                             p.in_ld * (int64_t)sizeof(T), Geo::NROWS);
+    if (!rc)
+      rc = encode_rows_map(&map.small, p.in, (int)sizeof(T), full_rows, p.batch,
+                           p.in_ld * (int64_t)sizeof(T), Geo::FROWS);
+    if (rc) return rc;
+    const WarpLB g = warp_geom<T>(p.batch, p.n, p.w);
+    if (!ws || ws_bytes < WarpWs<T>::bytes(g, p.batch)) return kErrWorkspace;
+    if (g.total > 0x7fffffffLL) return kErrUnsupported;
+    // every slot flag: one memset (32 B per 512 outputs)
+    cudaError_t e = cudaMemsetAsync(ws, 0, WarpWs<T>::bytes(g, p.batch), s);
+    if (e != cudaSuccess) return note_cuda(e);
+    // the far chunk's in-vector shift is a template parameter for 4-byte types
+    auto kern = k1d_warp<T, -1>;
+    if constexpr (sizeof(T) == 4) {
+      switch ((int)((p.w - 1) % Geo::VEC)) {
+        case 0: kern = k1d_warp<T, 0>; break;
+        case 1: kern = k1d_warp<T, 1>; break;
+        case 2: kern = k1d_warp<T, 2>; break;
+        default: kern = k1d_warp<T, 3>; break;
+      }
+    }
+    constexpr size_t smem = Geo::BYTES;
+    rc = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess
+             ? kOK
+             : note_cuda(cudaGetLastError());
+    if (rc) return rc;
+    int grid = 0;
+    rc = occupancy_grid(kern, smem, (g.total + NWARP - 1) / NWARP, grid);
+    if (rc) return rc;
+    kern<<<grid, NT, smem, s>>>(p, g, ws, map);
+    return note_cuda(cudaGetLastError());
+  }
+}
+
 // Batched 1-D filter (1-D is batch 1).  Arguments already validated.
 template <typename T>
 int launch_1d(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w, void *out_max,
@@ -248,6 +321,7 @@ int launch_1d(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w
     case Path1D::Small: return launch_small_dispatch<T>(p, map, s);
     case Path1D::Medium: return launch_medium<T>(p, map, s);
     case Path1D::Large: return launch_large<T>(p, map, ws, ws_bytes, s);
+    case Path1D::Warp: return launch_warp<T>(p, ws, ws_bytes, s);
     default: return kErrUnsupported;
   }
 }
