@@ -1,0 +1,19 @@
+# Round evidence: every bench config, the reference arm, the launch list of the
+# default bench, and ncu --set full captures of the kernels behind each config.
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem,power.draw --format=csv > gpurun_out/smi.txt 2>&1
+timeout 600 python bench.py > gpurun_out/bench_c2.log 2>&1; echo "rc=$?" >> gpurun_out/bench_c2.log
+for c in C1 C3 C4 C5; do
+  timeout 600 python bench.py --config $c --steps 20 > gpurun_out/bench_$c.log 2>&1; echo "rc=$?" >> gpurun_out/bench_$c.log
+done
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "rc=$?" >> gpurun_out/bench_ref.log
+timeout 300 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/plain_launch.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
+  python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_launch.log 2>&1
+for spec in "C2 3 k1d" "C2 32 k1d" "C2 1024 k1d" "C2 65536 k1d" "C3 129 k1d" "C4 15 k2d"; do
+  set -- $spec
+  timeout 200 python tools/prof_one.py --config $1 --w $2 --reps 2 > gpurun_out/plain_$1_$2.log 2>&1 && \
+  timeout 400 ncu --set full --clock-control none --import-source on -k regex:$3 -s 1 -c 1 -o gpurun_out/prof_$1_w$2 -f \
+    python tools/prof_one.py --config $1 --w $2 --reps 2 > gpurun_out/ncu_$1_$2.log 2>&1
+done
