@@ -129,6 +129,27 @@ def _run_1d(name: str, a, w: int):
     return mx, mn, Stats(int(st.comparisons), int(st.peak_wedge))
 
 
+def _run_arg(name: str, a, w: int):
+    a = np.ascontiguousarray(a)
+    n = a.shape[0]
+    m = max(n - w + 1, 0)
+    mx, mn = np.empty(m, a.dtype), np.empty(m, a.dtype)
+    ax, an = np.empty(m, np.int64), np.empty(m, np.int64)
+    _check(_fn(name, a.dtype)(_ptr(a), ctypes.c_int64(n), ctypes.c_int64(w), _ptr(mx), _ptr(mn),
+                              _ptr(ax), _ptr(an)))
+    return mx, mn, ax, an
+
+
+def arg_brute(a, w: int):
+    """N1 arg filter, the definition: (max, min, argmax, argmin), earliest positions."""
+    return _run_arg("arg_brute", a, w)
+
+
+def arg_wedge(a, w: int):
+    """N1 arg filter by the paper's wedge with equal values kept (earliest positions)."""
+    return _run_arg("arg_wedge", a, w)
+
+
 def brute_1d(a, w: int):
     """O1, the definition.  Returns (max, min, Stats)."""
     return _run_1d("brute_1d", a, w)

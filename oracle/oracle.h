@@ -22,6 +22,10 @@
  *                          1-D filter.
  *   oracle_batched_*      oracle_appendix_* on each row of a batch.
  *   oracle_windows_at_*   brute force for a list of window starts (spot checks).
+ *   oracle_arg_brute_*    N1 arg filter, the definition: earliest position of
+ *                          each window's max and min (reading R17).
+ *   oracle_arg_wedge_*    N1 arg filter by the paper's wedge (PAPER.md:364-401,
+ *                          locations PAPER.md:522-525) with equal values kept.
  *
  * Comparison counting follows PAPER.md:73-75: only value-vs-value comparisons
  * (a<b or b<a) are counted; index tests and deque bookkeeping are free.
@@ -75,7 +79,11 @@ typedef struct {
                               T *out_max, T *out_min);                          \
   int oracle_windows_at_##S(const T *a, int64_t n, int64_t w,                   \
                             const int64_t *starts, int64_t k, T *out_max,       \
-                            T *out_min);
+                            T *out_min);                                        \
+  int oracle_arg_brute_##S(const T *a, int64_t n, int64_t w, T *out_max,        \
+                           T *out_min, int64_t *arg_max, int64_t *arg_min);     \
+  int oracle_arg_wedge_##S(const T *a, int64_t n, int64_t w, T *out_max,        \
+                           T *out_min, int64_t *arg_max, int64_t *arg_min);
 
 ORACLE_DECLARE(u8, uint8_t)
 ORACLE_DECLARE(i8, int8_t)

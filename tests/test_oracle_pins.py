@@ -290,3 +290,47 @@ def test_errors():
         oracle.alg1(a, 1)  # reading R4: Algorithm 1 needs w >= 2
     with pytest.raises(oracle.OracleError):
         oracle.brute_2d(np.zeros((3, 3)), 4, 1)
+
+
+# ------------------------------------------------------------ N1: arg filter
+# Pins for oracle_arg_brute / oracle_arg_wedge: printed
+# examples, numpy's argmax/argmin (an independent implementation that returns
+# the FIRST occurrence -- the earliest-position rule R17), and the wedge equal
+# to the definition on every tiny case.
+
+def test_golden_arg_examples():
+    cases = json.load(open(os.path.join(GOLDEN, "examples_1d.json")))["arg_cases"]
+    for c in cases:
+        a = np.array(c["a"], np.int32)
+        for fn in (oracle.arg_brute, oracle.arg_wedge):
+            mx, mn, ax, an = fn(a, c["w"])
+            assert ax.tolist() == c["argmax"], (c["cite"], fn.__name__)
+            assert an.tolist() == c["argmin"], (c["cite"], fn.__name__)
+            assert mx.tolist() == a[ax].tolist() and mn.tolist() == a[an].tolist()
+
+
+@pytest.mark.parametrize("dtype", [np.uint8, np.int8, np.int16, np.uint32, np.int32, np.float32, np.float64])
+def test_arg_vs_numpy(dtype):
+    rng = np.random.default_rng(17)
+    for t in range(60):
+        n = int(rng.integers(1, 300))
+        w = int(rng.integers(1, n + 1))
+        a = synth.random_values(dtype, n, seed=500 + t, alphabet=(3 if t % 2 else None))
+        win = np.lib.stride_tricks.sliding_window_view(a, w)
+        base = np.arange(n - w + 1)
+        for fn in (oracle.arg_brute, oracle.arg_wedge):
+            mx, mn, ax, an = fn(a, w)
+            assert np.array_equal(ax, base + win.argmax(axis=1)), (t, fn.__name__)
+            assert np.array_equal(an, base + win.argmin(axis=1)), (t, fn.__name__)
+            assert np.array_equal(mx, win.max(axis=1)) and np.array_equal(mn, win.min(axis=1))
+
+
+def test_arg_wedge_equals_brute_exhaustive():
+    for n in range(1, 8):
+        for code in range(3 ** n):
+            a = np.array([(code // 3 ** k) % 3 for k in range(n)], np.int32)
+            for w in range(1, n + 1):
+                b = oracle.arg_brute(a, w)
+                g = oracle.arg_wedge(a, w)
+                for x, y in zip(b, g):
+                    assert np.array_equal(x, y), (a.tolist(), w)
