@@ -142,6 +142,29 @@ int maxmin_filter_2d(int dt, const void *in, int64_t batch, int64_t rows,
                      void *stream);
 
 /*
+ * Arg-max / arg-min filter (the paper keeps the locations
+ * of the extrema).  For every window j of every row:
+ *   out_max[j], out_min[j]  as maxmin_filter_batched,
+ *   arg_max[j], arg_min[j]  the absolute position (0-based, in [j, j+w)) of
+ *                           the max / min in the row; ties -> the EARLIEST
+ *                           position, for both (reading R17).
+ *   Any of the four outputs may be NULL (at least one must not be); all four
+ *   use the row pitch out_ld (elements).  Value outputs need element
+ *   alignment, position outputs (int64) 8-byte alignment; in needs element
+ *   alignment.  dtypes of <= 4 bytes (else MAXMIN_ERR_UNSUPPORTED) and
+ *   n < 2^32.  Workspace: maxmin_argfilter_workspace_bytes (~32 bytes per
+ *   element: the 64-bit (value, position) keys and their filtered copies).
+ *   Runs as keys -> max/min filters on the keys -> decode, all on the device.
+ */
+int maxmin_argfilter_workspace_bytes(int dt, int64_t batch, int64_t n, int64_t w,
+                                     size_t *bytes);
+int maxmin_argfilter_batched(int dt, const void *in, int64_t batch, int64_t n,
+                             int64_t in_ld, int64_t w, void *out_max,
+                             void *out_min, int64_t *arg_max, int64_t *arg_min,
+                             int64_t out_ld, void *workspace,
+                             size_t workspace_bytes, void *stream);
+
+/*
  * End-to-end 1-D call on HOST buffers (in, out_max, out_min are host
  * pointers; page-locked memory gives full PCIe bandwidth).  The input is
  * streamed to the device in chunks (with a (w-1)-element overlap), filtered

@@ -19,7 +19,8 @@ from ._lib import MaxMinError
 __all__ = [
     "MaxMinError", "dtype_code", "maxmin_workspace_bytes", "maxmin_filter_1d",
     "maxmin_filter_batched", "maxmin_filter_2d", "maxmin_filter_1d_host",
-    "maxmin_host_workspace_bytes", "version",
+    "maxmin_host_workspace_bytes", "maxmin_argfilter_workspace_bytes", "maxmin_argfilter_batched",
+    "maxmin_argfilter_1d", "version",
 ]
 
 _CODES = {
@@ -136,6 +137,46 @@ def maxmin_filter_2d(x: torch.Tensor, w_row: int, w_col: int, cols: int | None =
         out_max = out_max[0] if out_max is not None and out_max.dim() == 3 else out_max
         out_min = out_min[0] if out_min is not None and out_min.dim() == 3 else out_min
     return out_max, out_min
+
+
+def maxmin_argfilter_workspace_bytes(dtype, batch: int, n: int, w: int) -> int:
+    out = ctypes.c_size_t(0)
+    _lib.check(_lib.lib().maxmin_argfilter_workspace_bytes(dtype_code(dtype), batch, n, w, ctypes.byref(out)))
+    return int(out.value)
+
+
+def maxmin_argfilter_batched(x: torch.Tensor, w: int, n: int | None = None, *, want_max=True, want_min=True,
+                             values=True, workspace=None, stream=None):
+    """Arg-max / arg-min filter on every row of a 2-D CUDA tensor [batch, ld] (first n
+    columns): returns (out_max, out_min, arg_max, arg_min), positions int64 and absolute
+    in the row, ties resolved to the earliest position (N1)."""
+    if x.dim() != 2 or not x.is_cuda or x.stride(1) != 1:
+        raise ValueError("maxmin_argfilter_batched: x must be a row-major 2-D CUDA tensor")
+    batch, ncols = x.shape
+    n = ncols if n is None else n
+    m = max(n - w + 1, 0)
+    mk = lambda dt: torch.empty(batch, max(m, 1), dtype=dt, device=x.device)[:, :m]  # noqa: E731
+    out_max = mk(x.dtype) if want_max and values else None
+    out_min = mk(x.dtype) if want_min and values else None
+    arg_max = mk(torch.int64) if want_max else None
+    arg_min = mk(torch.int64) if want_min else None
+    need = maxmin_argfilter_workspace_bytes(x.dtype, batch, n, w)
+    if workspace is None:
+        workspace = torch.empty(max(need, 16), dtype=torch.uint8, device=x.device)
+    out_ld = max(m, 1)
+    _lib.check(_lib.lib().maxmin_argfilter_batched(
+        dtype_code(x.dtype), _ptr(x), batch, n, x.stride(0), w, _ptr(out_max), _ptr(out_min),
+        _ptr(arg_max), _ptr(arg_min), out_ld, _ptr(workspace), workspace.numel() * workspace.element_size(),
+        _stream_ptr(stream)))
+    return out_max, out_min, arg_max, arg_min
+
+
+def maxmin_argfilter_1d(x: torch.Tensor, w: int, **kw):
+    """Arg-max / arg-min filter of a contiguous 1-D CUDA tensor (see maxmin_argfilter_batched)."""
+    if x.dim() != 1 or not x.is_cuda or not x.is_contiguous():
+        raise ValueError("maxmin_argfilter_1d: x must be a contiguous 1-D CUDA tensor")
+    outs = maxmin_argfilter_batched(x[None], w, **kw)
+    return tuple(o[0] if o is not None else None for o in outs)
 
 
 def maxmin_host_workspace_bytes(dtype, n: int, w: int, chunk: int = 0) -> int:

@@ -26,6 +26,12 @@ int sm_count();                // SMs of the current device (cached)
 int launch_2d_byte(bool is_signed, const void *in, int64_t batch, int64_t rows, int64_t cols,
                    int64_t in_ld, int64_t in_bstride, int64_t w_row, int64_t w_col, void *out_max,
                    void *out_min, int64_t out_ld, int64_t out_bstride, cudaStream_t s);
+// arg-max / arg-min filter (argfilter.cu): <= 4-byte element types
+size_t argfilter_workspace(int64_t batch, int64_t n, int64_t w);
+template <typename T>
+int launch_argfilter(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w, void *out_max,
+                     void *out_min, int64_t *arg_max, int64_t *arg_min, int64_t out_ld, void *ws,
+                     size_t ws_bytes, cudaStream_t s);
 int encode_u8_map(CUtensorMap *map, const void *base, const int64_t dims[3], const int64_t strides[2],
                   const int box[3]);  // maxmin_abi.cu
 int encode_rows_map(CUtensorMap *map, const void *in, int elem_bytes, int64_t rows_per_series,

@@ -265,6 +265,71 @@ int maxmin_filter_1d(int dt, const void *in, int64_t n, int64_t w, void *out_max
                                workspace_bytes, stream);
 }
 
+// ------------------------------------------------------------ N1: arg filter
+int maxmin_argfilter_workspace_bytes(int dt, int64_t batch, int64_t n, int64_t w, size_t *bytes) {
+  if (!bytes) return MAXMIN_ERR_NULL;
+  *bytes = 0;
+  const size_t sz = maxmin_dtype_size(dt);
+  if (!sz) return MAXMIN_ERR_DTYPE;
+  if (sz > 4) return MAXMIN_ERR_UNSUPPORTED;
+  if (w < 1) return MAXMIN_ERR_WINDOW;
+  if (n < 1 || batch < 0) return MAXMIN_ERR_SHAPE;
+  if (w > n) return MAXMIN_ERR_WINDOW_TOO_LARGE;
+  if (n > 0xffffffffLL) return MAXMIN_ERR_UNSUPPORTED;  // positions travel as 32 bits
+  *bytes = mm::argfilter_workspace(batch, n, w);
+  return MAXMIN_OK;
+}
+
+int maxmin_argfilter_batched(int dt, const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w,
+                             void *out_max, void *out_min, int64_t *arg_max, int64_t *arg_min,
+                             int64_t out_ld, void *workspace, size_t workspace_bytes, void *stream) {
+  const size_t sz = maxmin_dtype_size(dt);
+  if (!sz) return MAXMIN_ERR_DTYPE;
+  if (!in || (!out_max && !out_min && !arg_max && !arg_min)) return MAXMIN_ERR_NULL;
+  if (w < 1) return MAXMIN_ERR_WINDOW;
+  if (n < 1 || batch < 0) return MAXMIN_ERR_SHAPE;
+  if (w > n) return MAXMIN_ERR_WINDOW_TOO_LARGE;
+  size_t need = 0;
+  int rc = maxmin_argfilter_workspace_bytes(dt, batch, n, w, &need);
+  if (rc != MAXMIN_OK) return rc;
+  const int64_t m = n - w + 1;
+  if (in_ld < n || out_ld < m) return MAXMIN_ERR_SHAPE;
+  size_t ib, ob, ab;
+  if (!extent(batch, n, in_ld, sz, &ib) || !extent(batch, m, out_ld, sz, &ob) ||
+      !extent(batch, m, out_ld, 8, &ab))
+    return MAXMIN_ERR_SHAPE;
+  auto el = [](const void *q, uintptr_t a) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) % a) == 0; };
+  if (!el(in, sz) || !el(out_max, sz) || !el(out_min, sz) || !el(arg_max, 8) || !el(arg_min, 8))
+    return MAXMIN_ERR_ALIGNMENT;
+  if (!workspace || workspace_bytes < need || !aligned16(workspace)) return MAXMIN_ERR_WORKSPACE;
+  if (batch == 0) return MAXMIN_OK;
+  const void *outs[4] = {out_max, out_min, arg_max, arg_min};
+  const size_t obytes[4] = {ob, ob, ab, ab};
+  for (int i = 0; i < 4; ++i) {
+    if (!outs[i]) continue;
+    if (overlap(in, ib, outs[i], obytes[i]) || overlap(workspace, need, outs[i], obytes[i]))
+      return MAXMIN_ERR_ALIAS;
+    for (int k = i + 1; k < 4; ++k)
+      if (outs[k] && overlap(outs[i], obytes[i], outs[k], obytes[k])) return MAXMIN_ERR_ALIAS;
+  }
+  if (overlap(workspace, need, in, ib)) return MAXMIN_ERR_ALIAS;
+  if ((rc = ensure_device(in)) != MAXMIN_OK) return rc;
+  for (int i = 0; i < 4; ++i)
+    if (outs[i] && (rc = ensure_device(outs[i])) != MAXMIN_OK) return rc;
+  if ((rc = ensure_device(workspace)) != MAXMIN_OK) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  switch (dt) {
+    case MAXMIN_U8: return mm::launch_argfilter<uint8_t>(in, batch, n, in_ld, w, out_max, out_min, arg_max, arg_min, out_ld, workspace, workspace_bytes, s);
+    case MAXMIN_I8: return mm::launch_argfilter<int8_t>(in, batch, n, in_ld, w, out_max, out_min, arg_max, arg_min, out_ld, workspace, workspace_bytes, s);
+    case MAXMIN_U16: return mm::launch_argfilter<uint16_t>(in, batch, n, in_ld, w, out_max, out_min, arg_max, arg_min, out_ld, workspace, workspace_bytes, s);
+    case MAXMIN_I16: return mm::launch_argfilter<int16_t>(in, batch, n, in_ld, w, out_max, out_min, arg_max, arg_min, out_ld, workspace, workspace_bytes, s);
+    case MAXMIN_U32: return mm::launch_argfilter<uint32_t>(in, batch, n, in_ld, w, out_max, out_min, arg_max, arg_min, out_ld, workspace, workspace_bytes, s);
+    case MAXMIN_I32: return mm::launch_argfilter<int32_t>(in, batch, n, in_ld, w, out_max, out_min, arg_max, arg_min, out_ld, workspace, workspace_bytes, s);
+    case MAXMIN_F32: return mm::launch_argfilter<float>(in, batch, n, in_ld, w, out_max, out_min, arg_max, arg_min, out_ld, workspace, workspace_bytes, s);
+    default: return MAXMIN_ERR_UNSUPPORTED;
+  }
+}
+
 int maxmin_filter_2d(int dt, const void *in, int64_t batch, int64_t rows, int64_t cols, int64_t in_ld,
                      int64_t in_bstride, int64_t w_row, int64_t w_col, void *out_max, void *out_min,
                      int64_t out_ld, int64_t out_bstride, void *stream) {

@@ -109,3 +109,21 @@ def test_binding_raises_without_fallback():
 
     with pytest.raises((ValueError, mm.MaxMinError, RuntimeError)):
         mm.maxmin_filter_1d(torch.zeros(100), 3)  # CPU tensor: no CPU path exists
+
+
+def test_argfilter_argument_errors(L):
+    """N1 entry points: every argument error is reported before any launch."""
+    b = ctypes.c_size_t(0)
+    assert L.maxmin_argfilter_workspace_bytes(8, 1, 1000, 10, ctypes.byref(b)) == 0 and b.value > 32 * 990
+    assert L.maxmin_argfilter_workspace_bytes(9, 1, 1000, 10, ctypes.byref(b)) == 10  # f64: unsupported
+    assert L.maxmin_argfilter_workspace_bytes(8, 1, 10, 0, ctypes.byref(b)) == 3
+    assert L.maxmin_argfilter_workspace_bytes(8, 1, 10, 11, ctypes.byref(b)) == 4
+    assert L.maxmin_argfilter_workspace_bytes(12, 1, 10, 3, ctypes.byref(b)) == 2
+    f = L.maxmin_argfilter_batched
+    P = 1 << 30  # fake addresses: every error below is found before any access
+    assert f(8, None, 1, 100, 100, 10, P + (1 << 24), None, None, None, 91, P + (1 << 26), 1 << 20, None) == 1
+    assert f(8, P, 1, 100, 100, 10, None, None, None, None, 91, P + (1 << 26), 1 << 20, None) == 1
+    assert f(8, P, 1, 100, 100, 10, None, None, P + (1 << 24) + 4, None, 91, P + (1 << 26), 1 << 20, None) == 6
+    assert f(8, P, 1, 100, 100, 10, None, None, P + (1 << 24), None, 91, None, 0, None) == 8
+    assert f(8, P, 1, 100, 100, 10, None, None, P + 8, None, 91, P + (1 << 26), 1 << 20, None) == 7
+    assert f(9, P, 1, 100, 100, 10, None, None, P + (1 << 24), None, 91, P + (1 << 26), 1 << 20, None) == 10

@@ -329,3 +329,52 @@ def test_2d_byte_strided_single_output(cuda_device):
     assert_same(ox[:, :, :C].contiguous(), ex)
     assert_same(on[:, :, :C].contiguous(), en)
     assert int(ox[:, :, C:].sum()) == 0 and int(on[:, :, C:].sum()) == 0
+
+
+# ------------------------------------------------------- N1: arg filter ----
+ARG_DTYPES = [np.uint8, np.int8, np.uint16, np.int16, np.uint32, np.int32, np.float32]
+
+
+@pytest.mark.parametrize("dtype", ARG_DTYPES, ids=lambda d: np.dtype(d).name)
+def test_argfilter_every_dtype(cuda_device, dtype):
+    """Values and earliest positions of max/min vs the definition, with ties
+    (small alphabets) and every kernel path of the key filters."""
+    n = 20_003
+    for k, w in enumerate([1, 2, 3, 8, 9, 100, 1000, 5000, 9000]):
+        a = synth.random_values(dtype, n, seed=2000 + k, alphabet=(4 if k % 2 else None))
+        x = torch.from_numpy(a).to(dev())
+        mx, mn, ax, an = mm.maxmin_argfilter_1d(x, w)
+        ex, en, eax, ean = oracle.arg_wedge(a, w)
+        assert_same(mx, ex, f"{np.dtype(dtype).name} max w={w}")
+        assert_same(mn, en, f"{np.dtype(dtype).name} min w={w}")
+        assert_same(ax, eax, f"{np.dtype(dtype).name} argmax w={w}")
+        assert_same(an, ean, f"{np.dtype(dtype).name} argmin w={w}")
+
+
+def test_argfilter_brute_and_batched(cuda_device):
+    a = synth.random_values(np.float32, 3 * 2500, seed=31, alphabet=6).reshape(3, 2500)
+    x = torch.from_numpy(a).to(dev())
+    for w in (5, 77, 2500):
+        mx, mn, ax, an = mm.maxmin_argfilter_batched(x, w)
+        for r in range(3):
+            ex, en, eax, ean = oracle.arg_brute(a[r], w)
+            assert_same(ax[r], eax, f"row {r} argmax w={w}")
+            assert_same(an[r], ean, f"row {r} argmin w={w}")
+            assert_same(mx[r], ex)
+            assert_same(mn[r], en)
+    # one side only, positions only
+    _, _, ax, an = mm.maxmin_argfilter_batched(x, 77, want_min=False, values=False)
+    assert an is None
+    assert_same(ax[1], oracle.arg_brute(a[1], 77)[2])
+
+
+def test_argfilter_c2_full_size(cuda_device):
+    """C2's array (n = 2^28) at w = 1024: positions vs the wedge oracle."""
+    a = synth.c2(1 << 28)
+    x = torch.from_numpy(a).to(dev())
+    mx, mn, ax, an = mm.maxmin_argfilter_1d(x, 1024)
+    ex, en, eax, ean = oracle.arg_wedge(a, 1024)
+    assert_same(ax, eax, "argmax")
+    assert_same(an, ean, "argmin")
+    assert_same(mx, ex)
+    assert_same(mn, en)
