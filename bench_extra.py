@@ -1,5 +1,6 @@
-"""bench.py --config C1|C3|C4: the other BASELINE.json workloads (item-sharded,
-no communication).  Same JSON line schema as bench.py; imported by bench.py."""
+"""bench.py --config C1|C3|C4|N1: the other BASELINE.json workloads (item-sharded,
+no communication) and the NEXT rows of SURVEY.md §8(f) built so far.  Same JSON
+line schema as bench.py; imported by bench.py."""
 from __future__ import annotations
 
 import json
@@ -128,6 +129,50 @@ def run_extra(args, rank, world, local):
         ms, clk = _timed(step, steps, args.warmup, world, dev)
         sample = None
         windows = (w,)
+    elif cfg == "N1":
+        # SURVEY.md §8(f) N1 on C2's array: values and earliest positions of the
+        # max and min of every window, w = 1024
+        import ctypes
+
+        n, w = bench.CONFIGS["C2"]["n"], 1024
+        host = torch.empty(n, dtype=torch.float32).pin_memory()
+        synth.c2(n, stream=rank, out=host.numpy())
+        x = host.to(dev)
+        m = n - w + 1
+        ox = torch.empty(m, dtype=torch.float32, device=dev)
+        on = torch.empty_like(ox)
+        ax = torch.empty(m, dtype=torch.int64, device=dev)
+        an = torch.empty_like(ax)
+        need = mm.maxmin_argfilter_workspace_bytes(torch.float32, 1, n, w)
+        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        L = mm._lib.lib()
+        vp = ctypes.c_void_p
+
+        def step():
+            mm._lib.check(L.maxmin_argfilter_batched(
+                mm.dtype_code(torch.float32), vp(x.data_ptr()), 1, n, n, w, vp(ox.data_ptr()),
+                vp(on.data_ptr()), vp(ax.data_ptr()), vp(an.data_ptr()), m, vp(ws.data_ptr()), need,
+                vp(torch.cuda.current_stream().cuda_stream)))
+
+        nb = 4 * n + 2 * m * (4 + 8)  # the fused contract: input once, values + int64 positions
+        outs = 2 * m * world
+        steps = args.steps
+        name = ("N1: arg-max/arg-min filter on C2's fp32 random walk, n=2^28 per GPU, w=1024 "
+                "(values + int64 earliest positions)")
+        dtype = "f32"
+        l2 = "inputs (1 GiB per GPU) larger than the 126 MB L2"
+        step()
+        torch.cuda.synchronize()
+        import oracle
+
+        k = 1 << 22
+        ex, en, eax, ean = oracle.arg_wedge(host[:k].numpy(), w)
+        mk = k - w + 1
+        parity = bool(np.array_equal(ax[:mk].cpu().numpy(), eax) and np.array_equal(an[:mk].cpu().numpy(), ean)
+                      and np.array_equal(ox[:mk].cpu().numpy(), ex) and np.array_equal(on[:mk].cpu().numpy(), en))
+        ms, clk = _timed(step, steps, args.warmup, world, dev)
+        sample = None
+        windows = (w,)
     else:
         raise SystemExit(f"unknown config {cfg}")
 
@@ -147,7 +192,7 @@ def run_extra(args, rank, world, local):
                        "parallelism": f"item sharding, dp{world}" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_source": peak_src},
-            "cpu_baseline": cpu, "e2e": None, "gpu_launches": steps, "clocks": clk,
+            "cpu_baseline": cpu, "e2e": None, "gpu_launches": steps * (4 if cfg == "N1" else 1), "clocks": clk,
             "parity": {"bit_exact": parity},
         }
         print(json.dumps(line), flush=True)
