@@ -39,7 +39,10 @@ namespace mm {
 template <typename T>
 struct WarpGeo {
   static_assert(sizeof(T) <= 4, "packed 64-bit slots hold <= 4-byte values");
-  static constexpr int E = Chunk<T>::E;      // elements per lane
+#ifndef MM_WARP_E
+#define MM_WARP_E 16
+#endif
+  static constexpr int E = sizeof(T) == 4 ? MM_WARP_E : Chunk<T>::E;  // elements per lane
   static constexpr int WT = 32 * E;          // outputs per warp-tile
   static constexpr int K = NWARP;            // warp-tiles per ticket (one per warp)
   static constexpr int RW = Rowing<T>::RW;   // elements per 128-B row
@@ -114,7 +117,10 @@ __device__ __forceinline__ void lds_far(const unsigned char *buf, int pos, T (&v
 }
 
 template <typename T, int SH>
-__global__ void __launch_bounds__(NT, 2)
+#ifndef MM_WARP_MINB
+#define MM_WARP_MINB 2
+#endif
+__global__ void __launch_bounds__(NT, MM_WARP_MINB)
     k1d_warp(Rows p, WarpLB g, void *ws, const __grid_constant__ TmaMaps maps) {
   using Geo = WarpGeo<T>;
   constexpr int E = Geo::E, WT = Geo::WT, K = Geo::K, RW = Geo::RW;
