@@ -84,7 +84,7 @@ def build(force: bool = False) -> str:
         if os.path.getmtime(_LIB_PATH) >= max(os.path.getmtime(s) for s in src):
             return _LIB_PATH
     subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-shared", "-fPIC", "-o",
-                           _LIB_PATH, src[0]])
+                           _LIB_PATH, src[0], "-lm"])
     return _LIB_PATH
 
 
@@ -148,6 +148,26 @@ def arg_brute(a, w: int):
 def arg_wedge(a, w: int):
     """N1 arg filter by the paper's wedge with equal values kept (earliest positions)."""
     return _run_arg("arg_wedge", a, w)
+
+
+def keogh(c, q, r: int, brute: bool = False, envelope: bool = False):
+    """N3 LB_Keogh of every candidate row of c [batch, n] against the query q [n] with
+    warping radius r (float32 data, float64 bounds).  With envelope=True also returns
+    the clipped envelope (U, L) as [batch, n] float32 arrays."""
+    c = np.ascontiguousarray(c, dtype=np.float32)
+    if c.ndim == 1:
+        c = c[None]
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    batch, n = c.shape
+    lb = np.empty(batch, np.float64)
+    U = np.empty((batch, n), np.float32) if envelope else None
+    L = np.empty((batch, n), np.float32) if envelope else None
+    f = getattr(_load(), "oracle_keogh_brute_f32" if brute else "oracle_keogh_f32")
+    f.restype = ctypes.c_int
+    _check(f(_ptr(c), ctypes.c_int64(batch), ctypes.c_int64(n), ctypes.c_int64(n), _ptr(q), ctypes.c_int64(r),
+             _ptr(lb), ctypes.c_void_p(None) if U is None else _ptr(U),
+             ctypes.c_void_p(None) if L is None else _ptr(L)))
+    return (lb, U, L) if envelope else lb
 
 
 def brute_1d(a, w: int):

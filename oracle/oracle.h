@@ -26,6 +26,9 @@
  *                          each window's max and min (reading R17).
  *   oracle_arg_wedge_*    N1 arg filter by the paper's wedge (PAPER.md:364-401,
  *                          locations PAPER.md:522-525) with equal values kept.
+ *   oracle_keogh_f32      N3 LB_Keogh: envelope = the max-min filter with
+ *                          w = 2r+1 clipped at the ends, bound
+ *                          summed in double; _brute: every window clipped.
  *
  * Comparison counting follows PAPER.md:73-75: only value-vs-value comparisons
  * (a<b or b<a) are counted; index tests and deque bookkeeping are free.
@@ -97,6 +100,12 @@ ORACLE_DECLARE(f32, float)
 ORACLE_DECLARE(f64, double)
 
 #undef ORACLE_DECLARE
+
+/* N3 LB_Keogh (float candidates and query, double bound; N3, R18). */
+int oracle_keogh_f32(const float *c, int64_t batch, int64_t n, int64_t ld, const float *q,
+                     int64_t r, double *lb, float *U, float *L);
+int oracle_keogh_brute_f32(const float *c, int64_t batch, int64_t n, int64_t ld, const float *q,
+                           int64_t r, double *lb, float *U, float *L);
 
 #ifdef __cplusplus
 }

@@ -334,3 +334,65 @@ def test_arg_wedge_equals_brute_exhaustive():
                 g = oracle.arg_wedge(a, w)
                 for x, y in zip(b, g):
                     assert np.array_equal(x, y), (a.tolist(), w)
+
+
+# ------------------------------------------------------------ N3: LB_Keogh
+# Pins for oracle_keogh_f32: the envelope equals scipy's
+# maximum/minimum_filter1d with edge replication (an independent library
+# implementation of the clipped window, reading R18); the bound equals the
+# formula recomputed from that envelope; LB_Keogh lower-bounds the banded DTW
+# distance (its defining property, computed here by brute-force dynamic
+# programming); it is 0 against itself and non-increasing in r.
+
+def _dtw_band(a, b, r):
+    n = len(a)
+    D = np.full((n + 1, n + 1), np.inf)
+    D[0, 0] = 0.0
+    for i in range(1, n + 1):
+        for j in range(max(1, i - r), min(n, i + r) + 1):
+            d = (float(a[i - 1]) - float(b[j - 1])) ** 2
+            D[i, j] = d + min(D[i - 1, j], D[i, j - 1], D[i - 1, j - 1])
+    return np.sqrt(D[n, n])
+
+
+def test_keogh_envelope_vs_scipy_and_formula():
+    from scipy.ndimage import maximum_filter1d, minimum_filter1d
+    rng = np.random.default_rng(23)
+    for t in range(40):
+        n = int(rng.integers(1, 200))
+        r = int(rng.integers(0, n + 3))
+        c = rng.standard_normal((3, n)).astype(np.float32)
+        q = rng.standard_normal(n).astype(np.float32)
+        lb, U, L = oracle.keogh(c, q, r, envelope=True)
+        lbb = oracle.keogh(c, q, r, brute=True)
+        assert np.array_equal(lb, lbb)
+        for b in range(3):
+            eu = maximum_filter1d(c[b], size=2 * r + 1, mode="nearest")
+            el = minimum_filter1d(c[b], size=2 * r + 1, mode="nearest")
+            assert np.array_equal(U[b], eu) and np.array_equal(L[b], el), (t, n, r)
+            qd, ud, ld = q.astype(np.float64), eu.astype(np.float64), el.astype(np.float64)
+            s = np.where(qd > ud, (qd - ud) ** 2, np.where(qd < ld, (ld - qd) ** 2, 0.0)).sum()
+            assert abs(lb[b] - np.sqrt(s)) <= 1e-12 * max(1.0, np.sqrt(s))
+
+
+def test_keogh_lower_bounds_dtw():
+    rng = np.random.default_rng(29)
+    for t in range(60):
+        n = int(rng.integers(2, 40))
+        r = int(rng.integers(0, n))
+        a = np.cumsum(rng.standard_normal(n)).astype(np.float32)
+        b = np.cumsum(rng.standard_normal(n)).astype(np.float32)
+        lb = oracle.keogh(b[None], a, r)[0]  # envelope around the candidate b, query a
+        assert lb <= _dtw_band(a, b, r) * (1 + 1e-9) + 1e-12, (t, n, r)
+
+
+def test_keogh_identity_and_monotone_in_r():
+    c = synth.c3(rows=4, length=300)
+    for b in range(4):
+        assert oracle.keogh(c[b][None], c[b], 5)[0] == 0.0
+    q = synth.c3(rows=1, length=300, row0=99)[0]
+    prev = np.inf
+    for r in (0, 1, 2, 4, 8, 16, 64, 299):
+        lb = oracle.keogh(c, q, r)
+        assert np.all(lb <= prev)
+        prev = lb
