@@ -1,4 +1,4 @@
-"""bench.py --config C1|C3|C4|N1: the other BASELINE.json workloads (item-sharded,
+"""bench.py --config C1|C3|C4|N1|N3: the other BASELINE.json workloads (item-sharded,
 no communication) and the NEXT rows of SURVEY.md §8(f) built so far.  Same JSON
 line schema as bench.py; imported by bench.py."""
 from __future__ import annotations
@@ -129,6 +129,40 @@ def run_extra(args, rank, world, local):
         ms, clk = _timed(step, steps, args.warmup, world, dev)
         sample = None
         windows = (w,)
+    elif cfg == "N3":
+        # SURVEY.md §8(f) N3 on C3's candidates: LB_Keogh of every series against one
+        # query, envelope radius 64 (w = 129), the envelope never leaving the chip
+        B, n, w = synth.C3["batch"], synth.C3["n"], synth.C3["w"]
+        r = (w - 1) // 2
+        r0, r1 = shard.shard_items(B, world, rank)
+        rows = r1 - r0
+        host = torch.empty(rows, n, dtype=torch.float32).pin_memory()
+        synth.c3(rows=rows, row0=r0, out=host.numpy())
+        x = host.to(dev)
+        qh = synth.c3(rows=1, row0=B)[0]  # a series outside the candidate set
+        q = torch.from_numpy(qh).to(dev)
+        lb = torch.empty(rows, dtype=torch.float64, device=dev)
+
+        def step():
+            mm.maxmin_lb_keogh_batched(x, q, r, out=lb)
+
+        nb = 4 * rows * n + 8 * rows  # candidates once + one double per candidate
+        outs = B  # one bound per candidate (all ranks)
+        steps = args.steps
+        name = "N3: LB_Keogh of 65536 fp32 series x 4096 (C3) against one query, r=64 (w=129), sharded by series"
+        dtype = "f32"
+        l2 = "inputs (1 GiB) larger than the 126 MB L2"
+        step()
+        torch.cuda.synchronize()
+        import oracle
+
+        k = min(rows, 1024)
+        ref = oracle.keogh(host[:k].numpy(), qh, r)
+        got = lb[:k].cpu().numpy()
+        parity = bool(np.all(np.abs(got - ref) <= 1e-12 * np.maximum(1.0, np.abs(ref))))
+        ms, clk = _timed(step, steps, args.warmup, world, dev)
+        sample = None
+        windows = (w,)
     elif cfg == "N1":
         # SURVEY.md §8(f) N1 on C2's array: values and earliest positions of the
         # max and min of every window, w = 1024
@@ -178,6 +212,7 @@ def run_extra(args, rank, world, local):
 
     ms_step = ms / steps
     value = outs / (ms_step / 1e3)
+    unit = "bounds/s" if cfg == "N3" else bench.UNIT
     achieved = nb / (ms_step / 1e3) / 1e9
     if rank == 0:
         cpu = None
@@ -185,14 +220,15 @@ def run_extra(args, rank, world, local):
             cpu = bench.cpu_baseline(cfg, np.ascontiguousarray(sample).reshape(-1) if cfg != "C3" else sample,
                                      windows, None) if cfg == "C1" else _cpu_batched(sample, windows[0])
         line = {
-            "metric": bench.METRIC, "value": value, "unit": bench.UNIT, "n_gpus": world, "steps": steps,
+            "metric": bench.METRIC, "value": value, "unit": unit, "n_gpus": world, "steps": steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": dtype, "data": "synthetic",
             "config": {"workload": name, "l2": l2,
                        "parallelism": f"item sharding, dp{world}" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_source": peak_src},
-            "cpu_baseline": cpu, "e2e": None, "gpu_launches": steps * (4 if cfg == "N1" else 1), "clocks": clk,
+            "cpu_baseline": cpu, "e2e": None,
+            "gpu_launches": steps * {"N1": 4, "N3": 3}.get(cfg, 1), "clocks": clk,
             "parity": {"bit_exact": parity},
         }
         print(json.dumps(line), flush=True)

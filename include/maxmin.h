@@ -165,6 +165,23 @@ int maxmin_argfilter_batched(int dt, const void *in, int64_t batch, int64_t n,
                              size_t workspace_bytes, void *stream);
 
 /*
+ * LB_Keogh lower bound of the time-warping distance, fused with the envelope
+ * ([keogh2005eid]).  For every candidate
+ * row b (cand + b*ld, n float samples) against the query (n float samples)
+ * with warping radius r >= 0:
+ *   U_i, L_i = max, min of the row over [max(0,i-r), min(n-1,i+r)]
+ *             (the running max-min filter with w = 2r+1, clipped at the ends)
+ *   lb[b] = sqrt( sum_i (q_i > U_i) ? (q_i-U_i)^2 : (q_i < L_i) ? (L_i-q_i)^2 : 0 )
+ * computed in double (summation order unspecified).  The envelope is never
+ * stored.  dtype MAXMIN_F32 only; cand 16-byte aligned with 16-byte row
+ * pitch, query 4-byte aligned, lb (batch doubles, device) 8-byte aligned.
+ * 2r+1 <= 8193 or 2r+1 > n (else MAXMIN_ERR_UNSUPPORTED).  No workspace.
+ */
+int maxmin_lb_keogh_batched(int dt, const void *cand, int64_t batch, int64_t n,
+                            int64_t ld, const void *query, int64_t r, double *lb,
+                            void *stream);
+
+/*
  * End-to-end 1-D call on HOST buffers (in, out_max, out_min are host
  * pointers; page-locked memory gives full PCIe bandwidth).  The input is
  * streamed to the device in chunks (with a (w-1)-element overlap), filtered

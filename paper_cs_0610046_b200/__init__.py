@@ -20,7 +20,7 @@ __all__ = [
     "MaxMinError", "dtype_code", "maxmin_workspace_bytes", "maxmin_filter_1d",
     "maxmin_filter_batched", "maxmin_filter_2d", "maxmin_filter_1d_host",
     "maxmin_host_workspace_bytes", "maxmin_argfilter_workspace_bytes", "maxmin_argfilter_batched",
-    "maxmin_argfilter_1d", "version",
+    "maxmin_argfilter_1d", "maxmin_lb_keogh_batched", "version",
 ]
 
 _CODES = {
@@ -177,6 +177,22 @@ def maxmin_argfilter_1d(x: torch.Tensor, w: int, **kw):
         raise ValueError("maxmin_argfilter_1d: x must be a contiguous 1-D CUDA tensor")
     outs = maxmin_argfilter_batched(x[None], w, **kw)
     return tuple(o[0] if o is not None else None for o in outs)
+
+
+def maxmin_lb_keogh_batched(cand: torch.Tensor, query: torch.Tensor, r: int, n: int | None = None, out=None,
+                            stream=None):
+    """LB_Keogh (N3) of every candidate row of a float32 CUDA tensor [batch, ld] (first n
+    columns) against the query (n floats), envelope radius r; returns float64 [batch]."""
+    if cand.dim() != 2 or not cand.is_cuda or cand.stride(1) != 1:
+        raise ValueError("maxmin_lb_keogh_batched: cand must be a row-major 2-D CUDA tensor")
+    batch, ncols = cand.shape
+    n = ncols if n is None else n
+    if query.dim() != 1 or not query.is_cuda or not query.is_contiguous() or query.shape[0] < n:
+        raise ValueError("maxmin_lb_keogh_batched: query must be a contiguous 1-D CUDA tensor of n samples")
+    lb = torch.empty(batch, dtype=torch.float64, device=cand.device) if out is None else out
+    _lib.check(_lib.lib().maxmin_lb_keogh_batched(dtype_code(cand.dtype), _ptr(cand), batch, n, cand.stride(0),
+                                                  _ptr(query), r, _ptr(lb), _stream_ptr(stream)))
+    return lb
 
 
 def maxmin_host_workspace_bytes(dtype, n: int, w: int, chunk: int = 0) -> int:

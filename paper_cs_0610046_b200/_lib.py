@@ -52,6 +52,7 @@ SIGNATURES = {
     "maxmin_argfilter_workspace_bytes": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i64, ctypes.POINTER(_sz)]),
     "maxmin_argfilter_batched": (ctypes.c_int, [ctypes.c_int, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp,
                                                 _vp, _i64, _vp, _sz, _vp]),
+    "maxmin_lb_keogh_batched": (ctypes.c_int, [ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _vp]),
     "maxmin_host_workspace_bytes": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i64, ctypes.POINTER(_sz)]),
     "maxmin_filter_1d_host": (ctypes.c_int, [ctypes.c_int, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _sz]),
 }

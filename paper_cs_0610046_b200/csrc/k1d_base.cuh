@@ -137,6 +137,17 @@ __device__ __forceinline__ void store_out(const Rows &p, int64_t row, int64_t j0
   }
 }
 
+// Epilogue of the 1-D kernels: what happens to a thread's E window results
+// (cnt <= 0: the thread's chunk lies past the tile's last window).  The
+// library's filters store them; N3 (keogh.cu) folds them into a bound instead.
+struct StoreEpi {
+  template <typename T, int E>
+  __device__ __forceinline__ void operator()(const Rows &p, int64_t row, int64_t j0, int cnt, const T (&ox)[E],
+                                             const T (&on)[E]) const {
+    if (cnt > 0) store_out<T, E>(p, row, j0, cnt, ox, on);
+  }
+};
+
 // max/min of v[o..E-1] for a warp-uniform (or single-lane) runtime o in [0, E)
 template <typename T, int E>
 __device__ __forceinline__ void suffix_from(const T (&v)[E], int o, T &hx, T &hn) {

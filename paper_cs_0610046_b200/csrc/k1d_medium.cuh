@@ -77,9 +77,9 @@ __device__ __forceinline__ void grp_scan_down(T &vx, T &vn, int gl) {
   }
 }
 
-template <typename T, int G>
+template <typename T, int G, class Epi = StoreEpi>
 __global__ void __launch_bounds__(NT, 2)
-    k1d_medium(Rows p, MedGeom g, const __grid_constant__ CUtensorMap map) {
+    k1d_medium(Rows p, MedGeom g, const __grid_constant__ CUtensorMap map, Epi epi = Epi()) {
   using Lay = MedLayout<T>;
   constexpr int E = Lay::E;
   constexpr int TILE = Lay::TILE;
@@ -263,14 +263,14 @@ __global__ void __launch_bounds__(NT, 2)
       cn = Ord<T>::mn(cn, mn);
     }
     const int c0 = tid * E;
-    if (c0 < tout) {
+    {
       T ox[E], on[E];
 #pragma unroll
       for (int k = 0; k < E; ++k) {
         ox[k] = Ord<T>::mx(ux[k], cx);
         on[k] = Ord<T>::mn(un[k], cn);
       }
-      store_out<T, E>(p, row, u0 + c0, tout - c0, ox, on);
+      epi(p, row, u0 + c0, tout - c0, ox, on);  // (every thread: the epilogue may be collective)
     }
     // No barrier needed before the next tile in steady state: stage st was last
     // read before this tile's barrier (the prefetch into it is issued after it),

@@ -19,8 +19,9 @@ struct SmallLayout {
   static constexpr size_t BYTES = 2 * (size_t)STAGE + 1024 + 64;
 };
 
-template <typename T, int W>
-__global__ void __launch_bounds__(NT) k1d_small(Rows p, const __grid_constant__ CUtensorMap map) {
+template <typename T, int W, class Epi = StoreEpi>
+__global__ void __launch_bounds__(NT) k1d_small(Rows p, const __grid_constant__ CUtensorMap map,
+                                                Epi epi = Epi()) {
   using Lay = SmallLayout<T, W>;
   constexpr int E = Lay::E;
   constexpr int VEC = Chunk<T>::VEC;
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(NT) k1d_small(Rows p, const __grid_constant__ 
     if (patch_tail<T>(p, X, row, u0, tout + W - 1, tid)) __syncthreads();
 
     const int c0 = tid * E;
-    if (c0 < tout) {
+    {  // every thread computes (lanes past tout on stale data): the epilogue may be collective
       T v[E + NXT];
       {
         T a[E], b[NXT];
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(NT) k1d_small(Rows p, const __grid_constant__ 
           on[j] = Ord<T>::mn(mn[j], mn[j + (W - SPAN)]);
         }
       }
-      store_out<T, E>(p, row, u0 + c0, tout - c0, ox, on);
+      epi(p, row, u0 + c0, tout - c0, ox, on);
     }
     __syncthreads();  // stage st is free for the prefetch of iteration it+1
   }

@@ -26,6 +26,9 @@ int sm_count();                // SMs of the current device (cached)
 int launch_2d_byte(bool is_signed, const void *in, int64_t batch, int64_t rows, int64_t cols,
                    int64_t in_ld, int64_t in_bstride, int64_t w_row, int64_t w_col, void *out_max,
                    void *out_min, int64_t out_ld, int64_t out_bstride, cudaStream_t s);
+// LB_Keogh fused with the envelope (keogh.cu): float rows
+int launch_keogh(const float *c, int64_t batch, int64_t n, int64_t ld, const float *q, int64_t r, double *lb,
+                 cudaStream_t s);
 // arg-max / arg-min filter (argfilter.cu): <= 4-byte element types
 size_t argfilter_workspace(int64_t batch, int64_t n, int64_t w);
 template <typename T>
@@ -112,46 +115,51 @@ static int set_smem(K kernel, size_t bytes, size_t &done) {
   return kOK;
 }
 
-template <typename T, int W>
-static int launch_small(const Rows &p, const CUtensorMap &map, cudaStream_t s) {
+template <typename T, int W, class Epi = StoreEpi>
+static int launch_small(const Rows &p, const CUtensorMap &map, cudaStream_t s, Epi epi = Epi()) {
   constexpr size_t smem = SmallLayout<T, W>::BYTES;
-  auto kern = k1d_small<T, W>;
+  auto kern = k1d_small<T, W, Epi>;
   static size_t attr = 0;
   int rc = set_smem(kern, smem, attr);
   if (rc) return rc;
   int grid = 0;
   rc = occupancy_grid(kern, smem, p.ntiles, grid);
   if (rc) return rc;
-  kern<<<grid, NT, smem, s>>>(p, map);
+  kern<<<grid, NT, smem, s>>>(p, map, epi);
   return note_cuda(cudaGetLastError());
 }
 
-template <typename T>
-static int launch_small_dispatch(const Rows &p, const CUtensorMap &map, cudaStream_t s) {
+template <typename T, class Epi = StoreEpi>
+static int launch_small_epi(const Rows &p, const CUtensorMap &map, cudaStream_t s, Epi epi = Epi()) {
   switch (p.w) {
-    case 2: return launch_small<T, 2>(p, map, s);
-    case 3: return launch_small<T, 3>(p, map, s);
-    case 4: return launch_small<T, 4>(p, map, s);
-    case 5: return launch_small<T, 5>(p, map, s);
-    case 6: return launch_small<T, 6>(p, map, s);
-    case 7: return launch_small<T, 7>(p, map, s);
-    case 8: return launch_small<T, 8>(p, map, s);
+    case 2: return launch_small<T, 2, Epi>(p, map, s, epi);
+    case 3: return launch_small<T, 3, Epi>(p, map, s, epi);
+    case 4: return launch_small<T, 4, Epi>(p, map, s, epi);
+    case 5: return launch_small<T, 5, Epi>(p, map, s, epi);
+    case 6: return launch_small<T, 6, Epi>(p, map, s, epi);
+    case 7: return launch_small<T, 7, Epi>(p, map, s, epi);
+    case 8: return launch_small<T, 8, Epi>(p, map, s, epi);
     default: break;
   }
   if constexpr (Chunk<T>::E == 16) {
     switch (p.w) {
-      case 9: return launch_small<T, 9>(p, map, s);
-      case 10: return launch_small<T, 10>(p, map, s);
-      case 11: return launch_small<T, 11>(p, map, s);
-      case 12: return launch_small<T, 12>(p, map, s);
-      case 13: return launch_small<T, 13>(p, map, s);
-      case 14: return launch_small<T, 14>(p, map, s);
-      case 15: return launch_small<T, 15>(p, map, s);
-      case 16: return launch_small<T, 16>(p, map, s);
+      case 9: return launch_small<T, 9, Epi>(p, map, s, epi);
+      case 10: return launch_small<T, 10, Epi>(p, map, s, epi);
+      case 11: return launch_small<T, 11, Epi>(p, map, s, epi);
+      case 12: return launch_small<T, 12, Epi>(p, map, s, epi);
+      case 13: return launch_small<T, 13, Epi>(p, map, s, epi);
+      case 14: return launch_small<T, 14, Epi>(p, map, s, epi);
+      case 15: return launch_small<T, 15, Epi>(p, map, s, epi);
+      case 16: return launch_small<T, 16, Epi>(p, map, s, epi);
       default: break;
     }
   }
   return kErrUnsupported;
+}
+
+template <typename T>
+static int launch_small_dispatch(const Rows &p, const CUtensorMap &map, cudaStream_t s) {
+  return launch_small_epi<T>(p, map, s);
 }
 
 // Block geometry of k1d_medium: B = E*G, the largest power of two <= w-1 with
@@ -181,9 +189,9 @@ MedGeom medium_geom(int64_t w, int G) {
   return g;
 }
 
-template <typename T, int G>
-static int launch_medium_g(const Rows &p, const CUtensorMap &map, cudaStream_t s) {
-  auto kern = k1d_medium<T, G>;
+template <typename T, int G, class Epi = StoreEpi>
+static int launch_medium_g(const Rows &p, const CUtensorMap &map, cudaStream_t s, Epi epi = Epi()) {
+  auto kern = k1d_medium<T, G, Epi>;
   static size_t attr = 0;
   const MedGeom g = medium_geom<T>(p.w, G);
   const size_t smem = MedLayout<T>::bytes(p.w, g.ring);
@@ -192,20 +200,25 @@ static int launch_medium_g(const Rows &p, const CUtensorMap &map, cudaStream_t s
   int grid = 0;
   rc = occupancy_grid(kern, smem, p.ntiles, grid);
   if (rc) return rc;
-  kern<<<grid, NT, smem, s>>>(p, g, map);
+  kern<<<grid, NT, smem, s>>>(p, g, map, epi);
   return note_cuda(cudaGetLastError());
+}
+
+template <typename T, class Epi = StoreEpi>
+static int launch_medium_epi(const Rows &p, const CUtensorMap &map, cudaStream_t s, Epi epi = Epi()) {
+  switch (medium_G<T>(p.w)) {
+    case 1: return launch_medium_g<T, 1, Epi>(p, map, s, epi);
+    case 2: return launch_medium_g<T, 2, Epi>(p, map, s, epi);
+    case 4: return launch_medium_g<T, 4, Epi>(p, map, s, epi);
+    case 8: return launch_medium_g<T, 8, Epi>(p, map, s, epi);
+    case 16: return launch_medium_g<T, 16, Epi>(p, map, s, epi);
+    default: return launch_medium_g<T, 32, Epi>(p, map, s, epi);
+  }
 }
 
 template <typename T>
 static int launch_medium(const Rows &p, const CUtensorMap &map, cudaStream_t s) {
-  switch (medium_G<T>(p.w)) {
-    case 1: return launch_medium_g<T, 1>(p, map, s);
-    case 2: return launch_medium_g<T, 2>(p, map, s);
-    case 4: return launch_medium_g<T, 4>(p, map, s);
-    case 8: return launch_medium_g<T, 8>(p, map, s);
-    case 16: return launch_medium_g<T, 16>(p, map, s);
-    default: return launch_medium_g<T, 32>(p, map, s);
-  }
+  return launch_medium_epi<T>(p, map, s);
 }
 
 template <typename T>

@@ -265,6 +265,30 @@ int maxmin_filter_1d(int dt, const void *in, int64_t n, int64_t w, void *out_max
                                workspace_bytes, stream);
 }
 
+// ------------------------------------------------------------ N3: LB_Keogh
+int maxmin_lb_keogh_batched(int dt, const void *cand, int64_t batch, int64_t n, int64_t ld, const void *query,
+                            int64_t r, double *lb, void *stream) {
+  if (!maxmin_dtype_size(dt)) return MAXMIN_ERR_DTYPE;
+  if (dt != MAXMIN_F32) return MAXMIN_ERR_UNSUPPORTED;
+  if (!cand || !query || !lb) return MAXMIN_ERR_NULL;
+  if (r < 0) return MAXMIN_ERR_WINDOW;
+  if (n < 1 || batch < 0 || ld < n) return MAXMIN_ERR_SHAPE;
+  if (2 * r + 1 <= n && 2 * r + 1 > mm::kHaloMax + 1) return MAXMIN_ERR_UNSUPPORTED;
+  size_t cb = 0;
+  if (!extent(batch, n, ld, 4, &cb)) return MAXMIN_ERR_SHAPE;
+  if (!aligned16(cand) || (batch > 1 && (ld * 4) % 16 != 0)) return MAXMIN_ERR_ALIGNMENT;
+  if (reinterpret_cast<uintptr_t>(query) % 4 || reinterpret_cast<uintptr_t>(lb) % 8) return MAXMIN_ERR_ALIGNMENT;
+  if (batch == 0) return MAXMIN_OK;
+  if (overlap(cand, cb, lb, (size_t)batch * 8) || overlap(query, (size_t)n * 4, lb, (size_t)batch * 8))
+    return MAXMIN_ERR_ALIAS;
+  int rc;
+  if ((rc = ensure_device(cand)) != MAXMIN_OK) return rc;
+  if ((rc = ensure_device(query)) != MAXMIN_OK) return rc;
+  if ((rc = ensure_device(lb)) != MAXMIN_OK) return rc;
+  return mm::launch_keogh(static_cast<const float *>(cand), batch, n, ld, static_cast<const float *>(query), r,
+                          lb, static_cast<cudaStream_t>(stream));
+}
+
 // ------------------------------------------------------------ N1: arg filter
 int maxmin_argfilter_workspace_bytes(int dt, int64_t batch, int64_t n, int64_t w, size_t *bytes) {
   if (!bytes) return MAXMIN_ERR_NULL;

@@ -378,3 +378,43 @@ def test_argfilter_c2_full_size(cuda_device):
     assert_same(an, ean, "argmin")
     assert_same(mx, ex)
     assert_same(mn, en)
+
+
+# ------------------------------------------------------------ N3: LB_Keogh ---
+def _keogh_close(got, exp):
+    got = got.cpu().numpy() if isinstance(got, torch.Tensor) else got
+    err = np.abs(got - exp) / np.maximum(1.0, np.abs(exp))
+    assert np.all(err <= 1e-12), (float(err.max()), int(err.argmax()))
+
+
+@pytest.mark.parametrize("r", [0, 1, 3, 7, 8, 40, 64, 300, 1000, 4096])
+def test_keogh_radii(cuda_device, r):
+    """Small (w <= 16), medium and clipped-only (2r+1 > n) paths, ragged rows."""
+    rows, n, ld = 19, 3001, 3004
+    c = synth.c3(rows=rows, length=n, ld=ld)
+    q = synth.c3(rows=1, length=n, row0=777)[0]
+    x = torch.from_numpy(c).to(dev())
+    qd = torch.from_numpy(q).to(dev())
+    lb = mm.maxmin_lb_keogh_batched(x, qd, r, n=n)
+    _keogh_close(lb, oracle.keogh(c[:, :n], q, r))
+
+
+def test_keogh_short_rows_and_identity(cuda_device):
+    for n in (1, 2, 5, 31, 33, 129):
+        ld = (n + 3) // 4 * 4  # 16-byte row pitch (the C ABI's rule)
+        c = synth.random_values(np.float32, 8 * ld, seed=n).reshape(8, ld)
+        q = synth.random_values(np.float32, n, seed=1000 + n)
+        for r in (0, 1, 2, 16, 64, 200):
+            lb = mm.maxmin_lb_keogh_batched(torch.from_numpy(c).to(dev()), torch.from_numpy(q).to(dev()), r, n=n)
+            _keogh_close(lb, oracle.keogh(c[:, :n], q, r))
+    c = synth.c3(rows=4, length=512)
+    lb = mm.maxmin_lb_keogh_batched(torch.from_numpy(c).to(dev()), torch.from_numpy(c[2].copy()).to(dev()), 64)
+    assert float(lb[2]) == 0.0
+
+
+def test_keogh_c3_shape_sample(cuda_device):
+    """C3's layout (4096-sample series, w = 129 -> r = 64) on a 4096-row slice."""
+    c = synth.c3(rows=4096, row0=4321)
+    q = synth.c3(rows=1, row0=65536)[0]
+    lb = mm.maxmin_lb_keogh_batched(torch.from_numpy(c).to(dev()), torch.from_numpy(q).to(dev()), 64)
+    _keogh_close(lb, oracle.keogh(c, q, 64))
