@@ -104,6 +104,29 @@ __device__ __forceinline__ void stage_tile(const Rows &p, const CUtensorMap *map
   }
 }
 
+// As stage_tile, with 32-row (4 KB) boxes for the bulk and 8-row boxes for the
+// rest: ~4x fewer TMA instructions for the issuing thread, whose warp would
+// otherwise reach the tile's CTA barrier late (k1d_medium).
+template <typename T>
+__device__ __forceinline__ void stage_tile2(const Rows &p, const TmaMaps *maps, unsigned char *buf, int64_t row,
+                                            int64_t u0, int64_t len, uint64_t *bar) {
+  constexpr int RW = Rowing<T>::RW;
+  if (!p.has_map) {
+    mbar_arrive_expect_tx(bar, 0);  // nothing in flight: the tail fix loads it all
+    return;
+  }
+  const int64_t r0 = u0 / RW;
+  const int64_t r1 = (u0 + len + RW - 1) / RW;
+  const int nrows = (int)(r1 - r0);
+  const int nbig = nrows / kBigRows;
+  const int nsmall = (nrows - nbig * kBigRows + kBoxRows - 1) / kBoxRows;
+  mbar_arrive_expect_tx(bar, (uint32_t)(nbig * kBigBytes + nsmall * kBoxBytes));
+  for (int k = 0; k < nbig; ++k) tma_box(&maps->big, buf + k * kBigBytes, (int)(r0 + k * kBigRows), (int)row, bar);
+  for (int k = 0; k < nsmall; ++k)
+    tma_box(&maps->small, buf + nbig * kBigBytes + k * kBoxBytes, (int)(r0 + nbig * kBigRows + k * kBoxRows),
+            (int)row, bar);
+}
+
 // Patch the partial last 128-B row (not covered by the tensor map); returns
 // whether shared memory was written (caller must __syncthreads()).
 template <typename T>

@@ -79,7 +79,7 @@ __device__ __forceinline__ void grp_scan_down(T &vx, T &vn, int gl) {
 
 template <typename T, int G, class Epi = StoreEpi>
 __global__ void __launch_bounds__(NT, 2)
-    k1d_medium(Rows p, MedGeom g, const __grid_constant__ CUtensorMap map, Epi epi = Epi()) {
+    k1d_medium(Rows p, MedGeom g, const __grid_constant__ TmaMaps maps, Epi epi = Epi()) {
   using Lay = MedLayout<T>;
   constexpr int E = Lay::E;
   constexpr int TILE = Lay::TILE;
@@ -114,14 +114,15 @@ __global__ void __launch_bounds__(NT, 2)
   nxt = cur;
 
   if (tid == 0) {
-    prefetch_tmap(&map);
+    prefetch_tmap(&maps.big);
+    prefetch_tmap(&maps.small);
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     fence_mbar_init();
   }
   __syncthreads();
   if (tid == 0 && t_begin < t_end)
-    stage_tile<T>(p, &map, stg(0), cur.row, cur.u0, cur.tout(p) + w - 1, &bars[0]);
+    stage_tile2<T>(p, &maps, stg(0), cur.row, cur.u0, cur.tout(p) + w - 1, &bars[0]);
 
   // H contribution of a chunk y (block-relative chunk gl) given its local max
   auto h_part = [&](const T (&y)[E], T ax, T an, T bl, T &hx, T &hn) {
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(NT, 2)
     const unsigned char *X = stg(st);
     nxt.advance(p);
     if (tid == 0 && t + 1 < t_end)  // prefetch the next tile into the other stage
-      stage_tile<T>(p, &map, stg(st ^ 1), nxt.row, nxt.u0, nxt.tout(p) + w - 1, &bars[st ^ 1]);
+      stage_tile2<T>(p, &maps, stg(st ^ 1), nxt.row, nxt.u0, nxt.tout(p) + w - 1, &bars[st ^ 1]);
     const int64_t row = cur.row, u0 = cur.u0;
     const int tout = cur.tout(p);
     const int64_t ab0 = u0 / B;  // far block index (within the row) of group 0

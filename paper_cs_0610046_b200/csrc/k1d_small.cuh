@@ -20,7 +20,7 @@ struct SmallLayout {
 };
 
 template <typename T, int W, class Epi = StoreEpi>
-__global__ void __launch_bounds__(NT) k1d_small(Rows p, const __grid_constant__ CUtensorMap map,
+__global__ void __launch_bounds__(NT) k1d_small(Rows p, const __grid_constant__ TmaMaps maps,
                                                 Epi epi = Epi()) {
   using Lay = SmallLayout<T, W>;
   constexpr int E = Lay::E;
@@ -38,7 +38,8 @@ __global__ void __launch_bounds__(NT) k1d_small(Rows p, const __grid_constant__ 
   const int tid = threadIdx.x;
 
   if (tid == 0) {
-    prefetch_tmap(&map);
+    prefetch_tmap(&maps.big);
+    prefetch_tmap(&maps.small);
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     fence_mbar_init();
@@ -50,14 +51,14 @@ __global__ void __launch_bounds__(NT) k1d_small(Rows p, const __grid_constant__ 
   cur.start(p, t_begin);
   nxt = cur;
   if (tid == 0 && t_begin < t_end)
-    stage_tile<T>(p, &map, stg(0), cur.row, cur.u0, cur.tout(p) + W - 1, &bars[0]);
+    stage_tile2<T>(p, &maps, stg(0), cur.row, cur.u0, cur.tout(p) + W - 1, &bars[0]);
   int it = 0;
   for (int64_t t = t_begin; t < t_end; ++t, ++it, cur = nxt) {
     const int st = it & 1;
     unsigned char *X = stg(st);
     nxt.advance(p);
     if (tid == 0 && t + 1 < t_end)  // prefetch the next tile into the other stage
-      stage_tile<T>(p, &map, stg(st ^ 1), nxt.row, nxt.u0, nxt.tout(p) + W - 1, &bars[st ^ 1]);
+      stage_tile2<T>(p, &maps, stg(st ^ 1), nxt.row, nxt.u0, nxt.tout(p) + W - 1, &bars[st ^ 1]);
     const int64_t row = cur.row, u0 = cur.u0;
     const int tout = cur.tout(p);
     mbar_wait(&bars[st], (it >> 1) & 1);

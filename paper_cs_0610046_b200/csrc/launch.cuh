@@ -116,7 +116,15 @@ static int set_smem(K kernel, size_t bytes, size_t &done) {
 }
 
 template <typename T, int W, class Epi = StoreEpi>
-static int launch_small(const Rows &p, const CUtensorMap &map, cudaStream_t s, Epi epi = Epi()) {
+static int launch_small(const Rows &p, const CUtensorMap &small, cudaStream_t s, Epi epi = Epi()) {
+  TmaMaps map;  // 8-row boxes (the caller's map) and 32-row boxes over the same rows
+  map.small = small;
+  std::memset(&map.big, 0, sizeof(map.big));
+  if (p.has_map) {
+    int rc = encode_rows_map(&map.big, p.in, (int)sizeof(T), p.n / Rowing<T>::RW, p.batch,
+                             p.in_ld * (int64_t)sizeof(T), kBigRows);
+    if (rc) return rc;
+  }
   constexpr size_t smem = SmallLayout<T, W>::BYTES;
   auto kern = k1d_small<T, W, Epi>;
   static size_t attr = 0;
@@ -190,7 +198,15 @@ MedGeom medium_geom(int64_t w, int G) {
 }
 
 template <typename T, int G, class Epi = StoreEpi>
-static int launch_medium_g(const Rows &p, const CUtensorMap &map, cudaStream_t s, Epi epi = Epi()) {
+static int launch_medium_g(const Rows &p, const CUtensorMap &small, cudaStream_t s, Epi epi = Epi()) {
+  TmaMaps map;  // 8-row boxes (the caller's map) and 32-row boxes over the same rows
+  map.small = small;
+  std::memset(&map.big, 0, sizeof(map.big));
+  if (p.has_map) {
+    int rc = encode_rows_map(&map.big, p.in, (int)sizeof(T), p.n / Rowing<T>::RW, p.batch,
+                             p.in_ld * (int64_t)sizeof(T), kBigRows);
+    if (rc) return rc;
+  }
   auto kern = k1d_medium<T, G, Epi>;
   static size_t attr = 0;
   const MedGeom g = medium_geom<T>(p.w, G);
