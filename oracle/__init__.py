@@ -19,6 +19,9 @@ cites the PAPER.md passage it follows:
 ``separable_2d``       rows then columns, PAPER.md:61-63
 ``batched``            ``appendix`` on every row
 ``windows_at``         brute force at a list of window starts
+``arg_brute/arg_wedge`` N1 arg filter (definition / wedge keeping ties, R17)
+``keogh``              N3 LB_Keogh (clipped envelope, R18)
+``Stream``             N2 one stream's wedge, zero-latency pushes (R19)
 =====================  ====================================================
 
 Parity pins live in ``tests/test_oracle_*.py``; none of the functions is
@@ -254,3 +257,52 @@ def windows_at(a, w: int, starts):
                                       _ptr(starts), ctypes.c_int64(starts.shape[0]), _ptr(mx),
                                       _ptr(mn)))
     return mx, mn
+
+
+class Stream:
+    """N2: one stream's monotonic wedge (Algorithm 1), fed by pushes
+    of any length; every window is returned by the push of its last sample (R19)."""
+
+    def __init__(self, dtype, w: int):
+        self.dtype = np.dtype(dtype)
+        self.w = w
+        self._h = ctypes.c_void_p()
+        _check(_fn("stream_new", self.dtype)(ctypes.c_int64(w), ctypes.byref(self._h)))
+        self._push = _fn("stream_push", self.dtype)
+
+    def push(self, x):
+        """Ingest the samples x; returns (max, min) of the windows they complete."""
+        x = np.ascontiguousarray(x, dtype=self.dtype)
+        c = x.shape[0]
+        mx, mn = np.empty(c, self.dtype), np.empty(c, self.dtype)
+        e = ctypes.c_int64(0)
+        _check(self._push(self._h, _ptr(x) if c else ctypes.c_void_p(None), ctypes.c_int64(c), _ptr(mx), _ptr(mn),
+                          ctypes.byref(e)))
+        return mx[:e.value], mn[:e.value]
+
+    def stats(self) -> Stats:
+        st = _Stats()
+        f = _load().oracle_stream_stats
+        f.restype = ctypes.c_int
+        _check(f(self._h, ctypes.byref(st)))
+        return Stats(int(st.comparisons), int(st.peak_wedge))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.oracle_stream_free(h)
+            self._h = ctypes.c_void_p()
+
+
+def stream_pushes(rows, w: int, sizes):
+    """N2 on many streams: rows [S, N] pushed in chunks of the given sizes (summing to
+    <= N); returns per push (out_max [S, e], out_min [S, e]) of the windows completed."""
+    rows = np.ascontiguousarray(rows)
+    streams = [Stream(rows.dtype, w) for _ in range(rows.shape[0])]
+    res, off = [], 0
+    for c in sizes:
+        outs = [s.push(rows[i, off:off + c]) for i, s in enumerate(streams)]
+        res.append((np.stack([o[0] for o in outs]) if outs else np.empty((0, 0), rows.dtype),
+                    np.stack([o[1] for o in outs]) if outs else np.empty((0, 0), rows.dtype)))
+        off += c
+    return res

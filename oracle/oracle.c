@@ -48,6 +48,30 @@ static void deque_pop_front(oracle_deque *d) {
   }
 }
 
+/* N2: the state of one stream (see oracle_stream_push_* in oracle_body.inc). */
+struct oracle_stream {
+  int64_t w, next;     /* window; position of the next sample */
+  oracle_deque U, L;   /* the wedge: stream positions */
+  void *ring;          /* the last w+1 values, position i at ring[i % (w+1)] */
+  uint64_t comparisons;
+  int64_t peak;
+};
+
+void oracle_stream_free(oracle_stream *s) {
+  if (!s) return;
+  deque_free(&s->U);
+  deque_free(&s->L);
+  free(s->ring);
+  free(s);
+}
+
+int oracle_stream_stats(const oracle_stream *s, oracle_stats *st) {
+  if (!s || !st) return ORACLE_ERR_SHAPE;
+  st->comparisons = s->comparisons;
+  st->peak_wedge = s->peak;
+  return ORACLE_OK;
+}
+
 #define T uint8_t
 #define S u8
 #include "oracle_body.inc"

@@ -61,6 +61,11 @@ typedef struct {
                         /* implicit newest element of the appendix variant)    */
 } oracle_stats;
 
+/* N2: one stream's wedge (opaque; oracle_stream_new_<S> / _push_<S> / _free). */
+typedef struct oracle_stream oracle_stream;
+void oracle_stream_free(oracle_stream *s);
+int oracle_stream_stats(const oracle_stream *s, oracle_stats *st);
+
 #define ORACLE_DECLARE(S, T)                                                    \
   int oracle_brute_1d_##S(const T *a, int64_t n, int64_t w, T *out_max,         \
                           T *out_min, oracle_stats *st);                        \
@@ -86,7 +91,10 @@ typedef struct {
   int oracle_arg_brute_##S(const T *a, int64_t n, int64_t w, T *out_max,        \
                            T *out_min, int64_t *arg_max, int64_t *arg_min);     \
   int oracle_arg_wedge_##S(const T *a, int64_t n, int64_t w, T *out_max,        \
-                           T *out_min, int64_t *arg_max, int64_t *arg_min);
+                           T *out_min, int64_t *arg_max, int64_t *arg_min);     \
+  int oracle_stream_new_##S(int64_t w, oracle_stream **out);                    \
+  int oracle_stream_push_##S(oracle_stream *s, const T *x, int64_t c,           \
+                             T *out_max, T *out_min, int64_t *emitted);
 
 ORACLE_DECLARE(u8, uint8_t)
 ORACLE_DECLARE(i8, int8_t)

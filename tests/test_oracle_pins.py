@@ -396,3 +396,85 @@ def test_keogh_identity_and_monotone_in_r():
         lb = oracle.keogh(c, q, r)
         assert np.all(lb <= prev)
         prev = lb
+
+
+# ---------------------------------------------------------------- N2 streaming
+def _stream_all(a, w, sizes, dtype=None):
+    s = oracle.Stream(np.asarray(a).dtype if dtype is None else dtype, w)
+    outs, off = [], 0
+    for c in sizes:
+        outs.append(s.push(np.asarray(a)[off:off + c]))
+        off += c
+    return s, outs
+
+
+def test_stream_spec_examples():
+    """SPEC.md:70-82: w=3 pushes 1,3,2 -> (3, 1) on the third push only; 2,2,2 -> (2, 2);
+    w=1 emits on the first push."""
+    s = oracle.Stream(np.int64, 3)
+    assert [len(s.push([v])[0]) for v in (1, 3)] == [0, 0]
+    mx, mn = s.push([2])
+    assert mx.tolist() == [3] and mn.tolist() == [1]
+    s = oracle.Stream(np.int64, 3)
+    mx, mn = s.push([2, 2, 2])
+    assert mx.tolist() == [2] and mn.tolist() == [2]
+    s = oracle.Stream(np.int64, 1)
+    mx, mn = s.push([5])
+    assert mx.tolist() == [5] and mn.tolist() == [5]
+
+
+def test_stream_exhaustive_tiny_zero_latency():
+    """Every {0,1,2}^n, n <= 6, every w, pushes of every composition of n into <= 3 parts:
+    concatenated emissions = the definition (numpy); each push emits exactly the windows
+    its samples complete (zero stream latency)."""
+    for n in range(1, 7):
+        comps = [(n,)] + [(k, n - k) for k in range(0, n + 1)] + [(1, k, n - 1 - k) for k in range(0, n)]
+        for a in itertools.product(range(3), repeat=n):
+            a = np.array(a, np.int32)
+            for w in range(1, n + 2):
+                for sizes in comps:
+                    _, outs = _stream_all(a, w, sizes)
+                    seen = 0
+                    for (mx, mn), c in zip(outs, sizes):
+                        want = max(0, seen + c - w + 1) - max(0, seen - w + 1)
+                        assert len(mx) == want, (a, w, sizes)
+                        seen += c
+                    got_x = np.concatenate([o[0] for o in outs])
+                    got_n = np.concatenate([o[1] for o in outs])
+                    if w <= n:
+                        ex, en = np_filter(a, w)
+                        assert same(got_x, ex) and same(got_n, en), (a, w, sizes)
+                    else:
+                        assert len(got_x) == 0
+
+
+@pytest.mark.parametrize("dtype", oracle.DTYPES)
+def test_stream_random_chunks_vs_numpy(dtype):
+    rng = np.random.default_rng(7)
+    a = synth.random_values(np.dtype(dtype), 3000, seed=11)
+    for w in (1, 2, 5, 64, 700):
+        sizes = rng.integers(0, 300, size=40)
+        sizes = sizes[np.cumsum(sizes) <= a.shape[0]]
+        n = int(sizes.sum())
+        _, outs = _stream_all(a, w, sizes.tolist())
+        ex, en = np_filter(a[:n], w)
+        assert same(np.concatenate([o[0] for o in outs]), ex)
+        assert same(np.concatenate([o[1] for o in outs]), en)
+
+
+@pytest.mark.parametrize("family", ["increasing", "decreasing", "alternating", "uniform"])
+def test_stream_comparison_and_wedge_bounds(family):
+    """Propositions PAPER.md:406-505 hold across push boundaries: <= 3n comparisons (<= 2n
+    on monotone input) and size(U)+size(L) <= w+1."""
+    n = 20000
+    rng = np.random.default_rng(3)
+    a = {"increasing": np.arange(n, dtype=np.float64), "decreasing": -np.arange(n, dtype=np.float64),
+         "alternating": (np.arange(n) % 2).astype(np.float64), "uniform": rng.random(n)}[family]
+    for w in (2, 3, 17, 1000):
+        sizes = [97] * (n // 97) + [n % 97]
+        s, _ = _stream_all(a, w, sizes)
+        st = s.stats()
+        assert st.comparisons <= 3 * n
+        if family in ("increasing", "decreasing"):
+            assert st.comparisons <= 2 * n
+        assert st.peak_wedge <= w + 1
