@@ -1,4 +1,4 @@
-"""bench.py --config C1|C3|C4|N1|N3: the other BASELINE.json workloads (item-sharded,
+"""bench.py --config C1|C3|C4|N1|N2|N3: the other BASELINE.json workloads (item-sharded,
 no communication) and the NEXT rows of SURVEY.md §8(f) built so far.  Same JSON
 line schema as bench.py; imported by bench.py."""
 from __future__ import annotations
@@ -45,6 +45,7 @@ def run_extra(args, rank, world, local):
 
     dev = torch.device("cuda", local)
     peak, peak_src = bench.load_peaks()
+    e2e = None
     cfg = args.config
     if cfg == "C1":
         n, w = synth.C1["n"], synth.C1["w"]
@@ -207,6 +208,69 @@ def run_extra(args, rank, world, local):
         ms, clk = _timed(step, steps, args.warmup, world, dev)
         sample = None
         windows = (w,)
+    elif cfg == "N2":
+        # C3's 65 536 series as online streams, w = 129, each step
+        # ingests the 4096 samples of every stream in 16 pushes of 256 (every push emits
+        # the 256 windows its samples complete); chunks resident in HBM, copied into the
+        # state by the push (chunk-pointer mode)
+        B, n, w = synth.C3["batch"], synth.C3["n"], synth.C3["w"]
+        c = 256
+        r0, r1 = shard.shard_items(B, world, rank)
+        rows = r1 - r0
+        host = torch.empty(rows, n, dtype=torch.float32).pin_memory()
+        synth.c3(rows=rows, row0=r0, out=host.numpy())
+        x = host.to(dev)
+        chunks = [x[:, p * c:(p + 1) * c].contiguous() for p in range(n // c)]
+        st = mm.MaxMinStream(torch.float32, rows, w, c, device=dev)
+        ox = torch.empty(rows, c, dtype=torch.float32, device=dev)
+        on = torch.empty_like(ox)
+        import oracle
+
+        k = min(rows, 256)
+        gx = np.empty((k, n - w + 1), np.float32)
+        gn = np.empty_like(gx)
+        j = 0
+        for ch in chunks:  # first pass: parity of every emitted window of k streams
+            _, _, fv = st.push(ch, out_max=ox, out_min=on)
+            e = c - fv
+            gx[:, j:j + e] = ox[:k, fv:].cpu().numpy()
+            gn[:, j:j + e] = on[:k, fv:].cpu().numpy()
+            j += e
+        ex, en = oracle.batched(host[:k].numpy(), w)
+        parity = bool(np.array_equal(gx, ex) and np.array_equal(gn, en))
+
+        def step():
+            for ch in chunks:
+                st.push(ch, out_max=ox, out_min=on)
+
+        # algorithmic bytes per stream and push: chunk in, 2 outputs, the w-1 state read + written
+        nb = 4 * rows * (n // c) * (3 * c + 2 * (w - 1))
+        outs = 2 * B * n  # every sample completes one window (streams past warm-up)
+        steps = args.steps
+        name = (f"N2: 65536 online fp32 streams (C3's series), w=129, 16 pushes x {c} samples per stream "
+                "per step, sharded by stream")
+        dtype = "f32"
+        l2 = "chunks (1 GiB per step) larger than the 126 MB L2"
+        ms, clk = _timed(step, steps, args.warmup, world, dev)
+        sample = None
+        windows = (w,)
+        # e2e: pinned host chunks -> device -> push -> outputs back to pinned host, per push
+        hchunks = [host[:, p * c:(p + 1) * c].contiguous().pin_memory() for p in range(n // c)]
+        dch = torch.empty(rows, c, dtype=torch.float32, device=dev)
+        hx = torch.empty(rows, c, dtype=torch.float32).pin_memory()
+        hn = torch.empty_like(hx).pin_memory()
+
+        def e2e_step():
+            for hc in hchunks:
+                dch.copy_(hc, non_blocking=True)
+                st.push(dch, out_max=ox, out_min=on)
+                hx.copy_(ox, non_blocking=True)
+                hn.copy_(on, non_blocking=True)
+
+        ems, _ = _timed(e2e_step, max(1, steps // 2), 1, world, dev)
+        e2e = {"value": outs / (ems / max(1, steps // 2) / 1e3), "unit": bench.UNIT,
+               "h2d_bytes_per_step": 4 * rows * n, "d2h_bytes_per_step": 8 * rows * n,
+               "path": "MaxMinStream.push per 256-sample chunk from pinned host, outputs back per push"}
     else:
         raise SystemExit(f"unknown config {cfg}")
 
@@ -227,8 +291,8 @@ def run_extra(args, rank, world, local):
                        "parallelism": f"item sharding, dp{world}" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_source": peak_src},
-            "cpu_baseline": cpu, "e2e": None,
-            "gpu_launches": steps * {"N1": 4, "N3": 3}.get(cfg, 1), "clocks": clk,
+            "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": steps * {"N1": 4, "N3": 3, "N2": 16}.get(cfg, 1), "clocks": clk,
             "parity": {"bit_exact": parity},
         }
         print(json.dumps(line), flush=True)

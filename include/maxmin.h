@@ -182,6 +182,58 @@ int maxmin_lb_keogh_batched(int dt, const void *cand, int64_t batch, int64_t n,
                             void *stream);
 
 /*
+ * Online multi-stream filter.  The paper's setting: a
+ * stream, filtered with zero stream latency ("the maximum number of data
+ * points required after the window has passed"; Table 1) and
+ * O(w) state.  `streams` independent streams ingest c
+ * samples each per push; a push emits, for every stream, the windows that its
+ * c new samples complete -- in the same call (reading R19).
+ *
+ * State: device memory of maxmin_stream_state_bytes(...) bytes, 16-byte
+ * aligned, owned by the caller, described by a host-side maxmin_stream that
+ * maxmin_stream_init fills in (it also zero-fills the device state on
+ * `stream`).  Per stream it holds the last w-1 samples (for E <= w-1 <= 1024,
+ * E = 16 elements, 8 for 8-byte types: two ping-pong rows, and a push is ONE
+ * kernel; otherwise a [history | max_chunk slot] row plus filter scratch, and
+ * a push is copy-in, filter, shift).  The struct is the caller's; push
+ * updates `seen` and `phase`.
+ *
+ * maxmin_stream_push(st, chunk, c, chunk_ld, out_max, out_min, out_ld,
+ *                    first_valid, stream):
+ *   0 <= c <= max_chunk new samples per stream from chunk, a device pointer
+ *   to [streams][chunk_ld] samples (element aligned, chunk_ld >= c; 16-byte
+ *   aligned rows are read with 16-byte copies).  out_max / out_min (either may
+ *   be NULL, not both): [streams][out_ld] device arrays, 16-byte aligned with
+ *   16-byte row pitch.  Column k in [0, c) receives the max / min of the w
+ *   samples ending at the k-th new sample, i.e. stream positions
+ *   [seen+k-w+1, seen+k]; columns k < *first_valid = clamp(w-1-seen, 0, c)
+ *   (the stream holds fewer than w samples there) are unspecified.  Then
+ *   st->seen += c.  Stream-ordered on `stream`: the chunk may be reused by
+ *   work ordered after the push.  c == 0 is a no-op.
+ *   Errors: MAXMIN_ERR_SHAPE (c out of range, ld), MAXMIN_ERR_ALIGNMENT,
+ *   MAXMIN_ERR_ALIAS (state, chunk and outputs must be disjoint).
+ */
+typedef struct maxmin_stream {
+  int32_t dtype;      /* maxmin_dtype */
+  int32_t phase;      /* which history buffer is current (fused path) */
+  int64_t streams;    /* independent streams */
+  int64_t w;          /* window */
+  int64_t max_chunk;  /* largest c of one push */
+  int64_t ld;         /* elements between state rows */
+  int64_t seen;       /* samples each stream has received */
+  void *state;        /* device buffer (caller-owned) */
+  size_t state_bytes;
+} maxmin_stream;
+
+int maxmin_stream_state_bytes(int dt, int64_t streams, int64_t w, int64_t max_chunk,
+                              size_t *bytes);
+int maxmin_stream_init(maxmin_stream *st, int dt, int64_t streams, int64_t w,
+                       int64_t max_chunk, void *state, size_t state_bytes, void *stream);
+int maxmin_stream_push(maxmin_stream *st, const void *chunk, int64_t c, int64_t chunk_ld,
+                       void *out_max, void *out_min, int64_t out_ld, int64_t *first_valid,
+                       void *stream);
+
+/*
  * End-to-end 1-D call on HOST buffers (in, out_max, out_min are host
  * pointers; page-locked memory gives full PCIe bandwidth).  The input is
  * streamed to the device in chunks (with a (w-1)-element overlap), filtered

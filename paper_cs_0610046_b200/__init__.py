@@ -20,7 +20,7 @@ __all__ = [
     "MaxMinError", "dtype_code", "maxmin_workspace_bytes", "maxmin_filter_1d",
     "maxmin_filter_batched", "maxmin_filter_2d", "maxmin_filter_1d_host",
     "maxmin_host_workspace_bytes", "maxmin_argfilter_workspace_bytes", "maxmin_argfilter_batched",
-    "maxmin_argfilter_1d", "maxmin_lb_keogh_batched", "version",
+    "maxmin_argfilter_1d", "maxmin_lb_keogh_batched", "maxmin_stream_state_bytes", "MaxMinStream", "version",
 ]
 
 _CODES = {
@@ -193,6 +193,68 @@ def maxmin_lb_keogh_batched(cand: torch.Tensor, query: torch.Tensor, r: int, n: 
     _lib.check(_lib.lib().maxmin_lb_keogh_batched(dtype_code(cand.dtype), _ptr(cand), batch, n, cand.stride(0),
                                                   _ptr(query), r, _ptr(lb), _stream_ptr(stream)))
     return lb
+
+
+def maxmin_stream_state_bytes(dtype, streams: int, w: int, max_chunk: int) -> int:
+    out = ctypes.c_size_t(0)
+    _lib.check(_lib.lib().maxmin_stream_state_bytes(dtype_code(dtype), streams, w, max_chunk, ctypes.byref(out)))
+    return int(out.value)
+
+
+class MaxMinStream:
+    """Online multi-stream filter (N2): `streams` independent streams with window w.
+
+    ``push(chunk)`` ingests chunk[:, :c] (a [streams, c] CUDA tensor, c <= max_chunk new
+    samples per stream) and returns (out_max, out_min, first_valid): column k holds the
+    window ending at the k-th new sample; columns < first_valid are not complete windows
+    yet (unspecified).  The state lives in one device tensor owned by this object.
+    """
+
+    def __init__(self, dtype, streams: int, w: int, max_chunk: int, device=None, stream=None):
+        device = torch.device("cuda") if device is None else torch.device(device)
+        self.dtype = dtype
+        nbytes = maxmin_stream_state_bytes(dtype, streams, w, max_chunk)
+        self.state = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)
+        self._st = _lib.Stream()
+        _lib.check(_lib.lib().maxmin_stream_init(ctypes.byref(self._st), dtype_code(dtype), streams, w, max_chunk,
+                                                 _ptr(self.state), nbytes, _stream_ptr(stream)))
+
+    @property
+    def seen(self) -> int:
+        return int(self._st.seen)
+
+    @property
+    def streams(self) -> int:
+        return int(self._st.streams)
+
+    @property
+    def w(self) -> int:
+        return int(self._st.w)
+
+    @property
+    def max_chunk(self) -> int:
+        return int(self._st.max_chunk)
+
+    def push(self, chunk: torch.Tensor, out_max=None, out_min=None, *, want_max=True, want_min=True,
+             stream=None):
+        if chunk.dim() != 2 or not chunk.is_cuda or chunk.stride(1) != 1 or chunk.shape[0] != self.streams:
+            raise ValueError("MaxMinStream.push: chunk must be a row-major [streams, c] CUDA tensor")
+        if chunk.dtype != self.dtype:
+            raise TypeError("MaxMinStream.push: chunk dtype differs from the stream's")
+        c = chunk.shape[1]
+        vec = max(16 // chunk.element_size(), 1)
+        c_pad = max((c + vec - 1) // vec * vec, vec)
+        if want_max and out_max is None:
+            out_max = torch.empty(self.streams, c_pad, dtype=self.dtype, device=chunk.device)[:, :c]
+        if want_min and out_min is None:
+            out_min = torch.empty(self.streams, c_pad, dtype=self.dtype, device=chunk.device)[:, :c]
+        om = out_max if out_max is not None else out_min
+        out_ld = om.stride(0) if om is not None else c_pad
+        fv = ctypes.c_int64(0)
+        _lib.check(_lib.lib().maxmin_stream_push(
+            ctypes.byref(self._st), _ptr(chunk), c, chunk.stride(0), _ptr(out_max), _ptr(out_min), out_ld,
+            ctypes.byref(fv), _stream_ptr(stream)))
+        return out_max, out_min, int(fv.value)
 
 
 def maxmin_host_workspace_bytes(dtype, n: int, w: int, chunk: int = 0) -> int:

@@ -38,6 +38,15 @@ _i64 = ctypes.c_int64
 _vp = ctypes.c_void_p
 _sz = ctypes.c_size_t
 
+
+class Stream(ctypes.Structure):
+    """maxmin_stream (include/maxmin.h): host-side description of N2 stream state."""
+    _fields_ = [("dtype", ctypes.c_int32), ("phase", ctypes.c_int32), ("streams", _i64), ("w", _i64),
+                ("max_chunk", _i64), ("ld", _i64), ("seen", _i64), ("state", _vp), ("state_bytes", _sz)]
+
+
+_sp = ctypes.POINTER(Stream)
+
 SIGNATURES = {
     "maxmin_status_str": (ctypes.c_char_p, [ctypes.c_int]),
     "maxmin_last_cuda_error": (ctypes.c_int, []),
@@ -53,6 +62,9 @@ SIGNATURES = {
     "maxmin_argfilter_batched": (ctypes.c_int, [ctypes.c_int, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp,
                                                 _vp, _i64, _vp, _sz, _vp]),
     "maxmin_lb_keogh_batched": (ctypes.c_int, [ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _vp]),
+    "maxmin_stream_state_bytes": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i64, ctypes.POINTER(_sz)]),
+    "maxmin_stream_init": (ctypes.c_int, [_sp, ctypes.c_int, _i64, _i64, _i64, _vp, _sz, _vp]),
+    "maxmin_stream_push": (ctypes.c_int, [_sp, _vp, _i64, _i64, _vp, _vp, _i64, ctypes.POINTER(_i64), _vp]),
     "maxmin_host_workspace_bytes": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i64, ctypes.POINTER(_sz)]),
     "maxmin_filter_1d_host": (ctypes.c_int, [ctypes.c_int, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _sz]),
 }

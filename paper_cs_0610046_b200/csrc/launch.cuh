@@ -35,6 +35,19 @@ template <typename T>
 int launch_argfilter(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w, void *out_max,
                      void *out_min, int64_t *arg_max, int64_t *arg_min, int64_t out_ld, void *ws,
                      size_t ws_bytes, cudaStream_t s);
+// online multi-stream filter (stream.cu)
+struct StreamLayout {
+  int fused;          // one fused kernel per push (ping-pong history rows) or the composition
+  int64_t ld;         // elements between state rows
+  size_t hist_bytes;  // one history buffer (fused) / the [history | slot] rows (composed)
+  size_t ws_bytes;    // the filter's workspace (composed)
+  size_t total;
+};
+template <typename T>
+StreamLayout stream_layout(int64_t streams, int64_t w, int64_t max_chunk);
+template <typename T>
+int launch_stream_push(void *state, const StreamLayout &L, int64_t streams, int64_t w, int phase, const T *chunk,
+                       int64_t c, int64_t chunk_ld, T *out_max, T *out_min, int64_t out_ld, cudaStream_t s);
 int encode_u8_map(CUtensorMap *map, const void *base, const int64_t dims[3], const int64_t strides[2],
                   const int box[3]);  // maxmin_abi.cu
 int encode_rows_map(CUtensorMap *map, const void *in, int elem_bytes, int64_t rows_per_series,

@@ -389,6 +389,100 @@ int maxmin_filter_2d(int dt, const void *in, int64_t batch, int64_t rows, int64_
                                           out_max, out_min, out_ld, out_bstride, s))
 }
 
+// ------------------------------------------------------------ N2: streams
+namespace {
+bool stream_lay(int dt, int64_t streams, int64_t w, int64_t max_chunk, mm::StreamLayout *L) {
+  const size_t sz = maxmin_dtype_size(dt);
+  if (w - 1 > INT64_MAX / 4 - max_chunk) return false;
+  size_t hb;
+  if (!extent(streams, w - 1 + max_chunk + 16, w - 1 + max_chunk + 16, sz, &hb)) return false;
+  MM_DISPATCH(dt, { *L = mm::stream_layout<T>(streams, w, max_chunk); return true; })
+}
+}  // namespace
+
+int maxmin_stream_state_bytes(int dt, int64_t streams, int64_t w, int64_t max_chunk, size_t *bytes) {
+  if (!bytes) return MAXMIN_ERR_NULL;
+  *bytes = 0;
+  if (!maxmin_dtype_size(dt)) return MAXMIN_ERR_DTYPE;
+  if (w < 1) return MAXMIN_ERR_WINDOW;
+  if (streams < 0 || max_chunk < 1) return MAXMIN_ERR_SHAPE;
+  mm::StreamLayout L;
+  if (!stream_lay(dt, streams, w, max_chunk, &L)) return MAXMIN_ERR_SHAPE;
+  *bytes = L.total;
+  return MAXMIN_OK;
+}
+
+int maxmin_stream_init(maxmin_stream *st, int dt, int64_t streams, int64_t w, int64_t max_chunk, void *state,
+                       size_t state_bytes, void *stream) {
+  if (!st) return MAXMIN_ERR_NULL;
+  size_t need = 0;
+  int rc = maxmin_stream_state_bytes(dt, streams, w, max_chunk, &need);
+  if (rc != MAXMIN_OK) return rc;
+  if (streams > 0 && !state) return MAXMIN_ERR_NULL;
+  if (state && !aligned16(state)) return MAXMIN_ERR_ALIGNMENT;
+  if (state_bytes < need) return MAXMIN_ERR_WORKSPACE;
+  mm::StreamLayout L;
+  stream_lay(dt, streams, w, max_chunk, &L);
+  st->dtype = dt;
+  st->phase = 0;
+  st->streams = streams;
+  st->w = w;
+  st->max_chunk = max_chunk;
+  st->ld = L.ld;
+  st->seen = 0;
+  st->state = state;
+  st->state_bytes = state_bytes;
+  if (streams == 0) return MAXMIN_OK;
+  if ((rc = ensure_device(state)) != MAXMIN_OK) return rc;
+  return mm::note_cuda(cudaMemsetAsync(state, 0, L.fused ? 2 * L.hist_bytes : L.hist_bytes,
+                                       static_cast<cudaStream_t>(stream)));
+}
+
+int maxmin_stream_push(maxmin_stream *st, const void *chunk, int64_t c, int64_t chunk_ld, void *out_max,
+                       void *out_min, int64_t out_ld, int64_t *first_valid, void *stream) {
+  if (!st || !first_valid) return MAXMIN_ERR_NULL;
+  const int dt = st->dtype;
+  const size_t sz = maxmin_dtype_size(dt);
+  if (!sz) return MAXMIN_ERR_DTYPE;
+  if (c < 0 || c > st->max_chunk || st->streams < 0 || st->w < 1) return MAXMIN_ERR_SHAPE;
+  mm::StreamLayout L;
+  if (!stream_lay(dt, st->streams, st->w, st->max_chunk, &L) || L.ld != st->ld || st->state_bytes < L.total)
+    return MAXMIN_ERR_SHAPE;
+  const int64_t h = st->w - 1;
+  const int64_t fv = h - st->seen;
+  *first_valid = fv < 0 ? 0 : (fv > c ? c : fv);
+  if (c == 0 || st->streams == 0) return MAXMIN_OK;
+  if (!st->state || !chunk || (!out_max && !out_min)) return MAXMIN_ERR_NULL;
+  if (out_ld < c || chunk_ld < c) return MAXMIN_ERR_SHAPE;
+  if (!aligned16(out_max) && out_max) return MAXMIN_ERR_ALIGNMENT;
+  if (!aligned16(out_min) && out_min) return MAXMIN_ERR_ALIGNMENT;
+  if (st->streams > 1 && ((size_t)out_ld * sz) % 16 != 0) return MAXMIN_ERR_ALIGNMENT;
+  if (reinterpret_cast<uintptr_t>(chunk) % sz != 0) return MAXMIN_ERR_ALIGNMENT;
+  size_t ob = 0, cb = 0;
+  if (!extent(st->streams, c, out_ld, sz, &ob) || !extent(st->streams, c, chunk_ld, sz, &cb)) return MAXMIN_ERR_SHAPE;
+  const void *regions[4] = {st->state, chunk, out_max, out_min};
+  const size_t rbytes[4] = {L.total, cb, ob, ob};
+  for (int i = 0; i < 4; ++i)
+    for (int k = i + 1; k < 4; ++k)
+      if (regions[i] && regions[k] && overlap(regions[i], rbytes[i], regions[k], rbytes[k])) return MAXMIN_ERR_ALIAS;
+  int rc;
+  if ((rc = ensure_device(st->state)) != MAXMIN_OK) return rc;
+  if ((rc = ensure_device(chunk)) != MAXMIN_OK) return rc;
+  if (out_max && (rc = ensure_device(out_max)) != MAXMIN_OK) return rc;
+  if (out_min && (rc = ensure_device(out_min)) != MAXMIN_OK) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  MM_DISPATCH(dt, {
+    rc = mm::launch_stream_push<T>(st->state, L, st->streams, st->w, st->phase, static_cast<const T *>(chunk), c,
+                                   chunk_ld, static_cast<T *>(out_max), static_cast<T *>(out_min), out_ld, s);
+    break;
+  })
+  if (rc == MAXMIN_OK) {
+    st->seen += c;
+    if (L.fused) st->phase ^= 1;
+  }
+  return rc;
+}
+
 // ------------------------------------------------------------ host pipeline
 static int64_t default_chunk(int64_t chunk) { return chunk > 0 ? chunk : (int64_t(1) << 24); }
 

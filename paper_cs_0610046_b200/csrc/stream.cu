@@ -1,0 +1,510 @@
+// stream.cu -- online multi-stream filter.
+//
+// The paper's setting is a stream: "the stream latency of a filter [is] the
+// maximum number of data points required after the window has passed"
+// (PAPER.md:68-72), and the monotonic wedge reaches latency 0 with O(w) state
+// (Table 1).  On the GPU, thousands of independent streams
+// ingest a chunk of c samples each per call, and every window that a chunk
+// completes is emitted by that same call (reading R19): zero latency per
+// push.  The state of a stream is its last w-1 samples (the wedge's value
+// buffer; the extrema are rebuilt from them and the chunk on every push).
+//
+// Two paths, chosen by w when the state is created:
+//
+// fused (E <= w-1 <= kStreamHMax; k_stream_fused): ONE kernel per push reads
+//   each stream's history and its new chunk, writes the c windows and the new
+//   history -- exactly the algorithmic bytes: c + 2c + 2(w-1) per stream.
+//   History rows are kept right-aligned in ping-pong buffers of hld =
+//   round_up(w-1, 16 B) elements, so the virtual row V' = [hist row | chunk]
+//   is 16-B aligned in both parts; window k starts at V'[P + k], P = hld-(w-1).
+//   Warps are autonomous: a warp owns a segment of 32E windows of one stream,
+//   stages V'[j0, j0 + P + 32E + w - 1) into its own 128B-swizzled buffer with
+//   cp.async (double-buffered: the next segment's copy is in flight while this
+//   one computes) and runs the near/far block decomposition of k1d_medium
+//   (k1d_medium.cuh) within the warp: block B = E*G <= w-1, gap aggregates of
+//   the far blocks before the segment are reduced from the staged halo.  The
+//   warp holding a stream's last window writes the new history.
+//
+// composed (any other w): the state row is [history (w-1) | slot (max_chunk)];
+//   a push copies the chunk into the slot, runs the batched filter (any 1-D
+//   kernel) over [0, w-1+c) and moves the last w-1 samples to the front.
+//   HBM bytes: 2c + (w-1+c) + 2c + 2(w-1) per stream.
+#include "launch.cuh"
+
+namespace mm {
+
+// dst[e] = src[e] for e in [d0, d1), one warp; dst is 16-B aligned at element
+// 0 (stores are 16-B vectors where whole), src any element alignment.  Each
+// 32-vector step loads everything before storing anything, and steps ascend,
+// so an overlapping in-row move with src = dst + c (c > 0) is safe.
+template <typename T>
+__device__ __forceinline__ void warp_copy(T *dst, const T *src, int64_t d0, int64_t d1, int lane) {
+  constexpr int VEC = 16 / sizeof(T);
+  const int64_t v0 = d0 / VEC, v1 = (d1 + VEC - 1) / VEC;
+  for (int64_t vb = v0; vb < v1; vb += 32) {
+    const int64_t v = vb + lane;
+    const int64_t e0 = v * VEC;
+    const bool any = v < v1;
+    const bool full = any && e0 >= d0 && e0 + VEC <= d1;
+    T buf[VEC];
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) {
+      const int64_t e = e0 + k;
+      buf[k] = (any && e >= d0 && e < d1) ? src[e] : T(0);
+    }
+    __syncwarp();
+    if (full) {
+      uint4 u;
+      memcpy(&u, buf, 16);
+      *reinterpret_cast<uint4 *>(dst + e0) = u;
+    } else if (any) {
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) {
+        const int64_t e = e0 + k;
+        if (e >= d0 && e < d1) dst[e] = buf[k];
+      }
+    }
+  }
+}
+
+// Row r: state[r*ld + e] = src[r*src_ld + e - src_shift] for e in [d0, d1).
+// ordered: one warp per row walks the whole range in ascending steps (the
+// in-row shift with overlap); else every row is cut into segments that warps
+// copy independently.
+template <typename T>
+__global__ void __launch_bounds__(256) k_stream_copy(T *state, int64_t streams, int64_t ld, const T *src,
+                                                     int64_t src_ld, int64_t src_shift, int64_t d0, int64_t d1,
+                                                     int ordered) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int64_t SEG = 32 * VEC * 8;  // elements per independent segment (8 warp steps)
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // segments start at 16-B boundaries of the destination row
+  const int64_t a0 = d0 / VEC * VEC;
+  const int64_t nseg = ordered ? 1 : (d1 - a0 + SEG - 1) / SEG;
+  const int64_t items = streams * nseg;
+  for (int64_t it = warp; it < items; it += nwarps) {
+    const int64_t r = it / nseg, sg = it - r * nseg;
+    int64_t s0 = ordered ? d0 : a0 + sg * SEG, s1 = ordered ? d1 : s0 + SEG;
+    if (s0 < d0) s0 = d0;
+    if (s1 > d1) s1 = d1;
+    T *drow = state + r * ld;
+    const T *srow = src + r * src_ld - src_shift;
+    warp_copy<T>(drow, srow, s0, s1, lane);
+  }
+}
+
+
+// ============================================================ fused path
+constexpr int kStreamHMax = 1024;  // largest w-1 of the fused kernel
+constexpr int kStreamWarps = 4;    // warps per CTA (~136 registers: 3 CTAs per SM)
+
+template <typename T>
+struct StreamGeo {
+  static constexpr int E = Chunk<T>::E;
+  static constexpr int VEC = 16 / (int)sizeof(T);
+  static constexpr int SEG = 32 * E;  // windows per warp segment
+  static constexpr int AGG = 64;      // far-block aggregate slots per warp and kind
+  // staged elements: P + SEG + w - 1, plus the 16-B over-reads of lds_swz
+  __host__ __device__ static int stage_bytes(int w) {
+    const int elems = VEC + SEG + w - 1 + E + 2 * VEC;
+    const int bytes = elems * (int)sizeof(T);
+    return (bytes + 1023) / 1024 * 1024;
+  }
+  __host__ __device__ static int warp_bytes(int w) { return 2 * stage_bytes(w) + 4 * AGG * (int)sizeof(T); }
+  __host__ __device__ static size_t cta_bytes(int w) { return 1024 + (size_t)kStreamWarps * warp_bytes(w); }
+};
+
+struct StreamArgs {
+  const void *hist_in;  // [streams][hld]: the current history (right-aligned)
+  void *hist_out;       // [streams][hld]: receives the new history
+  const void *chunk;    // [streams][chunk_ld]: c new samples per stream
+  void *out_max;
+  void *out_min;
+  int64_t hld, chunk_ld, c, out_ld, streams;
+  int64_t segs_per_row, nseg;
+  int w, P;            // window; pad of the history rows
+  int qp, rp, V;       // gap geometry of block B = E*G (k1d_medium.cuh MedGeom)
+  int chunk_vec;       // chunk rows are 16-B aligned (else staged element-wise)
+  int stage_bytes, warp_bytes;
+};
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// Stage V'[j0, j0 + len) of `row` into the swizzled buffer X (logical index
+// i = V' index - j0).  j0 and hld are multiples of VEC, so every 16-B unit
+// comes from one source.
+template <typename T>
+__device__ __forceinline__ void stream_stage(const StreamArgs &a, unsigned char *X, int64_t row, int64_t j0,
+                                             int len, int lane) {
+  constexpr int VEC = 16 / (int)sizeof(T);
+  const T *hist = static_cast<const T *>(a.hist_in) + row * a.hld;
+  const T *chk = static_cast<const T *>(a.chunk) + row * a.chunk_ld;
+  const int nq = (len + VEC - 1) / VEC;
+  for (int q = lane; q < nq; q += 32) {
+    const int64_t v = j0 + (int64_t)q * VEC;
+    unsigned char *dst = X + swz(q);
+    if (v < a.hld) {
+      cp_async16(dst, hist + v);
+    } else if (a.chunk_vec && v - a.hld + VEC <= a.c) {
+      cp_async16(dst, chk + (v - a.hld));
+    } else {
+      T t[VEC];
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) {
+        const int64_t u = v - a.hld + k;
+        t[k] = u < a.c ? chk[u] : T(0);
+      }
+      uint4 u4;
+      memcpy(&u4, t, 16);
+      *reinterpret_cast<uint4 *>(dst) = u4;
+    }
+  }
+}
+
+template <typename T, int G>
+__global__ void __launch_bounds__(32 * kStreamWarps) k_stream_fused(StreamArgs a) {
+  using Geo = StreamGeo<T>;
+  constexpr int E = Geo::E;
+  constexpr int SEG = Geo::SEG;
+  constexpr int B = E * G;
+  constexpr int VEC = Geo::VEC;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *base = smem_align1024(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char *wb = base + warp * a.warp_bytes;
+  auto stg = [&](int i) { return wb + i * a.stage_bytes; };
+  T *Gx = reinterpret_cast<T *>(wb + 2 * a.stage_bytes);
+  T *Gn = Gx + Geo::AGG;
+  T *Hx = Gn + Geo::AGG;
+  T *Hn = Hx + Geo::AGG;
+  const int w = a.w, P = a.P;
+  const int gl = lane & (G - 1);
+  const int grp = lane / G;
+  const int glast = (lane & ~(G - 1)) + G - 1;
+  const int hstart = B - a.rp;
+  const int h_lane = hstart / E, h_off = hstart - (hstart / E) * E;
+  const int64_t gw = blockIdx.x * (int64_t)kStreamWarps + warp, nw = (int64_t)gridDim.x * kStreamWarps;
+
+  auto seg_pos = [&](int64_t sg, int64_t &row, int64_t &j0) {
+    row = sg / a.segs_per_row;
+    j0 = (sg - row * a.segs_per_row) * SEG;
+  };
+  auto seg_len = [&](int64_t j0) {  // staged elements of a segment
+    const int64_t want = (int64_t)P + SEG + w - 1;
+    const int64_t have = a.hld + a.c - j0;
+    return (int)(want < have ? want : have);
+  };
+  auto h_part = [&](const T (&y)[E], T ax, T an, T bl, T &hx, T &hn) {
+    hx = hn = bl;
+    if (a.rp > 0) {
+      if (gl > h_lane) {
+        hx = Ord<T>::mx(hx, ax);
+        hn = Ord<T>::mn(hn, an);
+      } else if (gl == h_lane) {
+        T vx, vn;
+        suffix_from<T, E>(y, h_off, vx, vn);
+        hx = Ord<T>::mx(hx, vx);
+        hn = Ord<T>::mn(hn, vn);
+      }
+    }
+  };
+
+  if (gw < a.nseg) {
+    int64_t row, j0;
+    seg_pos(gw, row, j0);
+    stream_stage<T>(a, stg(0), row, j0, seg_len(j0), lane);
+  }
+  cp_async_commit();
+  int it = 0;
+  for (int64_t sg = gw; sg < a.nseg; sg += nw, ++it) {
+    if (sg + nw < a.nseg) {  // the next segment's copy flies while this one computes
+      int64_t row, j0;
+      seg_pos(sg + nw, row, j0);
+      stream_stage<T>(a, stg((it + 1) & 1), row, j0, seg_len(j0), lane);
+    }
+    cp_async_commit();
+    cp_async_wait1();
+    __syncwarp();
+    const unsigned char *X = stg(it & 1);
+    int64_t row, j0;
+    seg_pos(sg, row, j0);
+    const int64_t left = a.c - j0;
+    const int cnt = left < SEG ? (int)left : SEG;
+
+    // ---- far chunk: prefix (k1d_medium.cuh, same names)
+    T ux[E], un[E];
+    T cx, cn;
+    {
+      T y[E];
+      lds_swz<T, E>(X, P + lane * E + w - 1, y);
+      ux[0] = un[0] = y[0];
+#pragma unroll
+      for (int k = 1; k < E; ++k) {
+        ux[k] = Ord<T>::mx(ux[k - 1], y[k]);
+        un[k] = Ord<T>::mn(un[k - 1], y[k]);
+      }
+      T hx, hn;
+      h_part(y, ux[E - 1], un[E - 1], __shfl_sync(0xffffffffu, y[E - 1], glast), hx, hn);
+      grp_reduce<T, G>(hx, hn);
+      T ax = ux[E - 1], an = un[E - 1];
+      grp_scan_up<T, G>(ax, an, gl);
+      cx = shfl_up(ax, 1);
+      cn = shfl_up(an, 1);
+      if (gl == 0) {
+        cx = y[0];
+        cn = y[0];
+      }
+      if (gl == G - 1) {
+        Gx[a.V + grp] = ax;
+        Gn[a.V + grp] = an;
+        Hx[a.V + grp] = hx;
+        Hn[a.V + grp] = hn;
+      }
+    }
+    // ---- near chunk: suffix
+    {
+      T x[E];
+      lds_swz<T, E>(X, P + lane * E, x);
+      T sx = x[E - 1], sn = x[E - 1];
+      ux[E - 1] = Ord<T>::mx(ux[E - 1], sx);
+      un[E - 1] = Ord<T>::mn(un[E - 1], sn);
+#pragma unroll
+      for (int k = E - 2; k >= 0; --k) {
+        sx = Ord<T>::mx(sx, x[k]);
+        sn = Ord<T>::mn(sn, x[k]);
+        ux[k] = Ord<T>::mx(ux[k], sx);
+        un[k] = Ord<T>::mn(un[k], sn);
+      }
+      T bx = sx, bn = sn;
+      grp_scan_down<T, G>(bx, bn, gl);
+      T ex = shfl_down(bx, 1), en = shfl_down(bn, 1);
+      if (gl == G - 1) {
+        ex = x[E - 1];
+        en = x[E - 1];
+      }
+      cx = Ord<T>::mx(cx, ex);
+      cn = Ord<T>::mn(cn, en);
+    }
+    // ---- far blocks before the segment (always: segments carry nothing)
+    if (a.V > 0) {
+      const int nv = a.V * G;
+      for (int r0 = 0; r0 < nv; r0 += 32) {
+        const int vc = r0 + lane;
+        const int vcc = vc < nv ? vc : nv - 1;
+        const int gv = vcc / G;
+        T y[E];
+        lds_swz<T, E>(X, P + (gv - a.V) * B + w - 1 + gl * E, y);
+        T ax = y[0], an = y[0];
+#pragma unroll
+        for (int k = 1; k < E; ++k) {
+          ax = Ord<T>::mx(ax, y[k]);
+          an = Ord<T>::mn(an, y[k]);
+        }
+        T hx, hn;
+        h_part(y, ax, an, __shfl_sync(0xffffffffu, y[E - 1], glast), hx, hn);
+        grp_reduce<T, G>(ax, an);
+        grp_reduce<T, G>(hx, hn);
+        if (vc < nv && gl == 0) {
+          Gx[gv] = ax;
+          Gn[gv] = an;
+          Hx[gv] = hx;
+          Hn[gv] = hn;
+        }
+      }
+    }
+    __syncwarp();
+    // ---- gap + out
+    if (a.qp > 0 || a.rp > 0) {
+      const int b0 = a.V + grp - a.qp - 1;  // far block F_{g-q'-1}
+      T mx, mn;
+      if (a.rp > 0) {
+        mx = Hx[b0];
+        mn = Hn[b0];
+      } else {
+        mx = Gx[b0 + 1];
+        mn = Gn[b0 + 1];
+      }
+      for (int s = 1; s <= a.qp; ++s) {
+        mx = Ord<T>::mx(mx, Gx[b0 + s]);
+        mn = Ord<T>::mn(mn, Gn[b0 + s]);
+      }
+      cx = Ord<T>::mx(cx, mx);
+      cn = Ord<T>::mn(cn, mn);
+    }
+    {
+      T ox[E], on[E];
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        ox[k] = Ord<T>::mx(ux[k], cx);
+        on[k] = Ord<T>::mn(un[k], cn);
+      }
+      const int c0 = lane * E;
+      if (c0 < cnt) {
+        T *omx = a.out_max ? static_cast<T *>(a.out_max) + row * a.out_ld + j0 + c0 : nullptr;
+        T *omn = a.out_min ? static_cast<T *>(a.out_min) + row * a.out_ld + j0 + c0 : nullptr;
+        if (c0 + E <= cnt) {
+          if (omx) store_chunk<T, E>(omx, ox);
+          if (omn) store_chunk<T, E>(omn, on);
+        } else {
+#pragma unroll
+          for (int k = 0; k < E; ++k)
+            if (c0 + k < cnt) {
+              if (omx) omx[k] = ox[k];
+              if (omn) omn[k] = on[k];
+            }
+        }
+      }
+    }
+    // ---- the stream's last segment writes its new history: V'[c + t], t < hld
+    if (left <= SEG) {
+      T *ho = static_cast<T *>(a.hist_out) + row * a.hld;
+      const int off = (int)(a.c - j0);
+      for (int t = lane * VEC; t < a.hld; t += 32 * VEC) {
+        T v[VEC];
+        lds_swz<T, VEC>(X, off + t, v);
+        uint4 u4;
+        memcpy(&u4, v, 16);
+        *reinterpret_cast<uint4 *>(ho + t) = u4;
+      }
+    }
+    __syncwarp();  // X is restaged two segments later; the aggregates next segment
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+namespace {
+int copy_grid(int64_t items) {
+  const int64_t blocks = (items + 7) / 8;  // 8 warps per block
+  const int64_t cap = (int64_t)sm_count() * 8;
+  return (int)(blocks < 1 ? 1 : (blocks < cap ? blocks : cap));
+}
+}  // namespace
+
+template <typename T>
+StreamLayout stream_layout(int64_t streams, int64_t w, int64_t max_chunk) {
+  constexpr int VEC = 16 / (int)sizeof(T);
+  auto up256 = [](size_t x) { return (x + 255) & ~size_t(255); };
+  StreamLayout L;
+  L.fused = (w - 1 >= StreamGeo<T>::E && w - 1 <= kStreamHMax) ? 1 : 0;
+  if (L.fused) {  // two history buffers (ping-pong), rows right-aligned
+    L.ld = (w - 1 + VEC - 1) / VEC * VEC;
+    L.hist_bytes = up256((size_t)streams * L.ld * sizeof(T));
+    L.ws_bytes = 0;
+    L.total = 2 * L.hist_bytes;
+  } else {  // [history | slot] rows + the filter's workspace
+    L.ld = (w - 1 + max_chunk + VEC - 1) / VEC * VEC;
+    L.hist_bytes = up256((size_t)streams * L.ld * sizeof(T));
+    L.ws_bytes = workspace_1d<T>(streams, w - 1 + max_chunk, w);
+    L.total = L.hist_bytes + up256(L.ws_bytes);
+  }
+  return L;
+}
+
+template <typename T, int G>
+int launch_fused_g(const StreamArgs &a, cudaStream_t s) {
+  const size_t smem = StreamGeo<T>::cta_bytes(a.w);
+  static int attr_set = 0;  // the largest dynamic smem size this instantiation was opened to
+  if ((int)smem > attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_stream_fused<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return note_cuda(e);
+    attr_set = (int)smem;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stream_fused<T, G>, 32 * kStreamWarps, smem);
+  if (e != cudaSuccess) return note_cuda(e);
+  if (per_sm < 1) return kErrUnsupported;
+  const int64_t want = (a.nseg + kStreamWarps - 1) / kStreamWarps;
+  const int64_t cap = (int64_t)sm_count() * per_sm;
+  const int grid = (int)(want < cap ? want : cap);
+  k_stream_fused<T, G><<<grid, 32 * kStreamWarps, smem, s>>>(a);
+  return note_cuda(cudaGetLastError());
+}
+
+template <typename T>
+int launch_stream_push(void *state, const StreamLayout &L, int64_t streams, int64_t w, int phase, const T *chunk,
+                       int64_t c, int64_t chunk_ld, T *out_max, T *out_min, int64_t out_ld, cudaStream_t s) {
+  if (streams == 0 || c == 0) return kOK;
+  constexpr int VEC = 16 / (int)sizeof(T);
+  const int64_t h = w - 1;
+  if (L.fused) {
+    using Geo = StreamGeo<T>;
+    char *base = static_cast<char *>(state);
+    StreamArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.hist_in = base + (phase ? L.hist_bytes : 0);
+    a.hist_out = base + (phase ? 0 : L.hist_bytes);
+    a.chunk = chunk;
+    a.out_max = out_max;
+    a.out_min = out_min;
+    a.hld = L.ld;
+    a.chunk_ld = chunk_ld;
+    a.c = c;
+    a.out_ld = out_ld;
+    a.streams = streams;
+    a.segs_per_row = (c + Geo::SEG - 1) / Geo::SEG;
+    a.nseg = streams * a.segs_per_row;
+    a.w = (int)w;
+    a.P = (int)(L.ld - h);
+    int G = 1;
+    while (G < 32 && Geo::E * G * 2 <= h) G *= 2;
+    const int B = Geo::E * G;
+    const int D = (int)h - B;
+    a.qp = D / B;
+    a.rp = D - a.qp * B;
+    a.V = a.qp + (a.rp > 0 ? 1 : 0);
+    if (a.V + 32 / G > Geo::AGG) return kErrUnsupported;
+    a.chunk_vec = (reinterpret_cast<uintptr_t>(chunk) % 16 == 0 && (chunk_ld * (int64_t)sizeof(T)) % 16 == 0) ? 1 : 0;
+    a.stage_bytes = Geo::stage_bytes((int)w);
+    a.warp_bytes = Geo::warp_bytes((int)w);
+    switch (G) {
+      case 1: return launch_fused_g<T, 1>(a, s);
+      case 2: return launch_fused_g<T, 2>(a, s);
+      case 4: return launch_fused_g<T, 4>(a, s);
+      case 8: return launch_fused_g<T, 8>(a, s);
+      case 16: return launch_fused_g<T, 16>(a, s);
+      default: return launch_fused_g<T, 32>(a, s);
+    }
+  }
+  T *rows = static_cast<T *>(state);
+  const int64_t ld = L.ld;
+  void *ws = L.ws_bytes ? static_cast<char *>(state) + L.hist_bytes : nullptr;
+  {  // 1. ingest into the slot [h, h+c)
+    const int64_t nseg = (h + c - h / VEC * VEC + 32 * VEC * 8 - 1) / (32 * VEC * 8);
+    k_stream_copy<T><<<copy_grid(streams * nseg), 256, 0, s>>>(rows, streams, ld, chunk, chunk_ld, h, h, h + c, 0);
+    int rc = note_cuda(cudaGetLastError());
+    if (rc) return rc;
+  }
+  // 2. the filter: rows of n = h + c samples, c windows each
+  int rc = launch_1d<T>(rows, streams, h + c, ld, w, out_max, out_min, out_ld, ws, L.ws_bytes, s);
+  if (rc) return rc;
+  if (h > 0) {  // 3. shift: [c, c+h) -> [0, h)
+    const bool ordered = c < h;
+    const int64_t items = ordered ? streams : streams * ((h + 32 * VEC * 8 - 1) / (32 * VEC * 8));
+    k_stream_copy<T><<<copy_grid(items), 256, 0, s>>>(rows, streams, ld, rows, ld, -c, 0, h, ordered ? 1 : 0);
+    rc = note_cuda(cudaGetLastError());
+  }
+  return rc;
+}
+
+#define MM_STREAM_INST(T)                                                                                      \
+  template StreamLayout stream_layout<T>(int64_t, int64_t, int64_t);                                           \
+  template int launch_stream_push<T>(void *, const StreamLayout &, int64_t, int64_t, int, const T *, int64_t,  \
+                                     int64_t, T *, T *, int64_t, cudaStream_t);
+MM_STREAM_INST(uint8_t)
+MM_STREAM_INST(int8_t)
+MM_STREAM_INST(uint16_t)
+MM_STREAM_INST(int16_t)
+MM_STREAM_INST(uint32_t)
+MM_STREAM_INST(int32_t)
+MM_STREAM_INST(uint64_t)
+MM_STREAM_INST(int64_t)
+MM_STREAM_INST(float)
+MM_STREAM_INST(double)
+
+}  // namespace mm

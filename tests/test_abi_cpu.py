@@ -127,3 +127,31 @@ def test_argfilter_argument_errors(L):
     assert f(8, P, 1, 100, 100, 10, None, None, P + (1 << 24), None, 91, None, 0, None) == 8
     assert f(8, P, 1, 100, 100, 10, None, None, P + 8, None, 91, P + (1 << 26), 1 << 20, None) == 7
     assert f(9, P, 1, 100, 100, 10, None, None, P + (1 << 24), None, 91, P + (1 << 26), 1 << 20, None) == 10
+
+
+def test_stream_argument_errors(L):
+    """N2 entry points: argument errors are reported before any CUDA call."""
+    from paper_cs_0610046_b200 import _lib
+
+    b = ctypes.c_size_t(0)
+    assert L.maxmin_stream_state_bytes(8, 65536, 129, 256, ctypes.byref(b)) == 0
+    assert b.value >= 2 * 65536 * 128 * 4  # fused path: two history rows of w-1 samples
+    assert L.maxmin_stream_state_bytes(12, 4, 3, 8, ctypes.byref(b)) == 2
+    assert L.maxmin_stream_state_bytes(8, 4, 0, 8, ctypes.byref(b)) == 3
+    assert L.maxmin_stream_state_bytes(8, 4, 3, 0, ctypes.byref(b)) == 5
+    assert L.maxmin_stream_state_bytes(8, -1, 3, 8, ctypes.byref(b)) == 5
+    st = _lib.Stream()
+    P = 1 << 30
+    L.maxmin_stream_state_bytes(8, 4, 3, 8, ctypes.byref(b))
+    assert L.maxmin_stream_init(None, 8, 4, 3, 8, P, b.value, None) == 1
+    assert L.maxmin_stream_init(ctypes.byref(st), 8, 4, 3, 8, None, b.value, None) == 1
+    assert L.maxmin_stream_init(ctypes.byref(st), 8, 4, 3, 8, P + 4, b.value, None) == 6
+    assert L.maxmin_stream_init(ctypes.byref(st), 8, 4, 3, 8, P, b.value - 1, None) == 8
+    # a zero-stream state needs no device memory: init and push are no-ops
+    assert L.maxmin_stream_init(ctypes.byref(st), 8, 0, 3, 8, None, 0, None) == 0
+    fv = ctypes.c_int64(-1)
+    assert L.maxmin_stream_push(ctypes.byref(st), None, 5, 0, None, None, 8, ctypes.byref(fv), None) == 0
+    assert fv.value == 2 and st.seen == 0  # w-1 = 2 samples short; nothing ingested with no streams
+    assert L.maxmin_stream_push(ctypes.byref(st), None, 9, 0, None, None, 8, ctypes.byref(fv), None) == 5
+    assert L.maxmin_stream_push(ctypes.byref(st), None, -1, 0, None, None, 8, ctypes.byref(fv), None) == 5
+    assert L.maxmin_stream_push(ctypes.byref(st), None, 1, 0, None, None, 8, None, None) == 1

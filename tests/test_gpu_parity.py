@@ -418,3 +418,74 @@ def test_keogh_c3_shape_sample(cuda_device):
     q = synth.c3(rows=1, row0=65536)[0]
     lb = mm.maxmin_lb_keogh_batched(torch.from_numpy(c).to(dev()), torch.from_numpy(q).to(dev()), 64)
     _keogh_close(lb, oracle.keogh(c, q, 64))
+
+
+# ------------------------------------------------------------- N2: streams
+def _stream_check(dtype, streams, w, sizes, max_chunk, seed, pitch=None):
+    N = int(sum(sizes))
+    rows = np.stack([synth.random_values(np.dtype(dtype), max(N, 1), seed=seed, stream=s)[:N]
+                     for s in range(streams)]) if streams else np.empty((0, N), dtype)
+    exp = oracle.stream_pushes(rows, w, sizes)
+    st = mm.MaxMinStream(torch.from_numpy(np.empty(0, dtype)).dtype, streams, w, max_chunk, device=dev())
+    x = torch.from_numpy(rows).to(dev())
+    off = 0
+    for p, c in enumerate(sizes):
+        if pitch is None:
+            ch = x[:, off:off + c].contiguous()
+        else:  # chunk rows at an odd pitch: element-wise staging
+            ch = torch.empty(streams, c + pitch, dtype=x.dtype, device=dev())[:, :c]
+            ch.copy_(x[:, off:off + c])
+        mx, mn, fv = st.push(ch)
+        torch.cuda.synchronize()
+        ex, en = exp[p]
+        e = ex.shape[1] if streams else max(0, min(c, off + c - w + 1))
+        assert fv == c - e, (p, c, fv, e)
+        if streams and e:
+            assert_same(mx[:, fv:], ex, f"max push {p} (c={c})")
+            assert_same(mn[:, fv:], en, f"min push {p} (c={c})")
+        off += c
+    assert st.seen == N
+
+
+@pytest.mark.parametrize("w", [1, 2, 3, 16, 17, 18, 33, 129, 200, 513, 600, 1000, 1025, 1026, 4097, 9000])
+def test_stream_pushes_f32(cuda_device, w):
+    rng = np.random.default_rng(w)
+    max_chunk = 1500
+    sizes = [0, 1, 2, min(w // 2, max_chunk), max_chunk, 3, w + 5 if w + 5 <= max_chunk else 700] + \
+        rng.integers(0, max_chunk + 1, size=8).tolist()
+    _stream_check(np.float32, 37, w, sizes, max_chunk, seed=w)
+
+
+@pytest.mark.parametrize("dtype", DTYPES, ids=lambda d: np.dtype(d).name)
+def test_stream_every_dtype(cuda_device, dtype):
+    for w in (5, 17, 300, 1025, 9000):
+        sizes = [100, 4000, 7, 2999, 4096, 1]
+        _stream_check(dtype, 9, w, sizes, 4096, seed=w + 1)
+
+
+def test_stream_odd_chunk_pitch(cuda_device):
+    _stream_check(np.float32, 64, 129, [256] * 6 + [13, 255], 256, seed=5, pitch=1)
+    _stream_check(np.uint8, 64, 40, [256] * 3 + [13, 255], 256, seed=6, pitch=3)
+
+
+def test_stream_c3_full_size(cuda_device):
+    """C3's 65 536 series as streams, 16 pushes of 256 samples, w=129 (the N2 bench
+    workload): every window against the oracle's batch filter on the whole rows
+    (streaming = batch) -- all rows, all windows."""
+    rows = synth.c3()
+    w, c = 129, 256
+    st = mm.MaxMinStream(torch.float32, rows.shape[0], w, c, device=dev())
+    x = torch.from_numpy(rows).to(dev())
+    gx = torch.empty(rows.shape[0], rows.shape[1] - w + 1, dtype=torch.float32)
+    gn = torch.empty_like(gx)
+    k = 0
+    for p in range(rows.shape[1] // c):
+        mx, mn, fv = st.push(x[:, p * c:(p + 1) * c].contiguous())
+        e = c - fv
+        gx[:, k:k + e] = mx[:, fv:].cpu()
+        gn[:, k:k + e] = mn[:, fv:].cpu()
+        k += e
+    assert k == rows.shape[1] - w + 1
+    ex, en = oracle.batched(rows, w)
+    assert_same(gx, ex, "C3 stream max")
+    assert_same(gn, en, "C3 stream min")
