@@ -22,6 +22,7 @@ cites the PAPER.md passage it follows:
 ``arg_brute/arg_wedge`` N1 arg filter (definition / wedge keeping ties, R17)
 ``keogh``              N3 LB_Keogh (clipped envelope, R18)
 ``Stream``             N2 one stream's wedge, zero-latency pushes (R19)
+``morph`` / ``morph_2d`` N4 opening and closing (definition or composition, R20)
 =====================  ====================================================
 
 Parity pins live in ``tests/test_oracle_*.py``; none of the functions is
@@ -306,3 +307,28 @@ def stream_pushes(rows, w: int, sizes):
                     np.stack([o[1] for o in outs]) if outs else np.empty((0, 0), rows.dtype)))
         off += c
     return res
+
+
+def morph(a, w: int, brute: bool = False):
+    """N4 grayscale (opening, closing) of a 1-D array by a flat segment of w samples
+    (reading R20); brute=True evaluates the definition, else the composition."""
+    a = np.ascontiguousarray(a)
+    n = a.shape[0]
+    op, cl = np.empty(n, a.dtype), np.empty(n, a.dtype)
+    _check(_fn("morph_brute" if brute else "morph", a.dtype)(_ptr(a), ctypes.c_int64(n), ctypes.c_int64(w),
+                                                             _ptr(op), _ptr(cl)))
+    return op, cl
+
+
+def morph_2d(a, w_row: int, w_col: int, brute: bool = False):
+    """N4 (opening, closing) of [batch,] rows x cols images by a flat w_col x w_row rectangle."""
+    a = np.ascontiguousarray(a)
+    squeeze = a.ndim == 2
+    if squeeze:
+        a = a[None]
+    batch, rows, cols = a.shape
+    op, cl = np.empty_like(a), np.empty_like(a)
+    _check(_fn("morph_2d_brute" if brute else "morph_2d", a.dtype)(
+        _ptr(a), ctypes.c_int64(batch), ctypes.c_int64(rows), ctypes.c_int64(cols), ctypes.c_int64(w_row),
+        ctypes.c_int64(w_col), _ptr(op), _ptr(cl)))
+    return (op[0], cl[0]) if squeeze else (op, cl)

@@ -73,55 +73,95 @@ int oracle_stream_stats(const oracle_stream *s, oracle_stats *st) {
 }
 
 #define T uint8_t
+#define TLOW 0
+#define THIGH UINT8_MAX
 #define S u8
 #include "oracle_body.inc"
 #undef T
 #undef S
+#undef TLOW
+#undef THIGH
 #define T int8_t
+#define TLOW INT8_MIN
+#define THIGH INT8_MAX
 #define S i8
 #include "oracle_body.inc"
 #undef T
 #undef S
+#undef TLOW
+#undef THIGH
 #define T uint16_t
+#define TLOW 0
+#define THIGH UINT16_MAX
 #define S u16
 #include "oracle_body.inc"
 #undef T
 #undef S
+#undef TLOW
+#undef THIGH
 #define T int16_t
+#define TLOW INT16_MIN
+#define THIGH INT16_MAX
 #define S i16
 #include "oracle_body.inc"
 #undef T
 #undef S
+#undef TLOW
+#undef THIGH
 #define T uint32_t
+#define TLOW 0
+#define THIGH UINT32_MAX
 #define S u32
 #include "oracle_body.inc"
 #undef T
 #undef S
+#undef TLOW
+#undef THIGH
 #define T int32_t
+#define TLOW INT32_MIN
+#define THIGH INT32_MAX
 #define S i32
 #include "oracle_body.inc"
 #undef T
 #undef S
+#undef TLOW
+#undef THIGH
 #define T uint64_t
+#define TLOW 0
+#define THIGH UINT64_MAX
 #define S u64
 #include "oracle_body.inc"
 #undef T
 #undef S
+#undef TLOW
+#undef THIGH
 #define T int64_t
+#define TLOW INT64_MIN
+#define THIGH INT64_MAX
 #define S i64
 #include "oracle_body.inc"
 #undef T
 #undef S
+#undef TLOW
+#undef THIGH
 #define T float
+#define TLOW (-INFINITY)
+#define THIGH INFINITY
 #define S f32
 #include "oracle_body.inc"
 #undef T
 #undef S
+#undef TLOW
+#undef THIGH
 #define T double
+#define TLOW (-INFINITY)
+#define THIGH INFINITY
 #define S f64
 #include "oracle_body.inc"
 #undef T
 #undef S
+#undef TLOW
+#undef THIGH
 
 /* ------------------------------------------------------------------ N3 ----
  * LB_Keogh (the max-min filter as the

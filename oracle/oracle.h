@@ -92,6 +92,15 @@ int oracle_stream_stats(const oracle_stream *s, oracle_stats *st);
                            T *out_min, int64_t *arg_max, int64_t *arg_min);     \
   int oracle_arg_wedge_##S(const T *a, int64_t n, int64_t w, T *out_max,        \
                            T *out_min, int64_t *arg_max, int64_t *arg_min);     \
+  int oracle_morph_brute_##S(const T *a, int64_t n, int64_t w, T *open,        \
+                             T *close);                                         \
+  int oracle_morph_##S(const T *a, int64_t n, int64_t w, T *open, T *close);    \
+  int oracle_morph_2d_brute_##S(const T *a, int64_t batch, int64_t rows,        \
+                                int64_t cols, int64_t w_row, int64_t w_col,     \
+                                T *open, T *close);                             \
+  int oracle_morph_2d_##S(const T *a, int64_t batch, int64_t rows,              \
+                          int64_t cols, int64_t w_row, int64_t w_col,           \
+                          T *open, T *close);                                   \
   int oracle_stream_new_##S(int64_t w, oracle_stream **out);                    \
   int oracle_stream_push_##S(oracle_stream *s, const T *x, int64_t c,           \
                              T *out_max, T *out_min, int64_t *emitted);

@@ -112,8 +112,8 @@ struct StreamGeo {
     const int bytes = elems * (int)sizeof(T);
     return (bytes + 1023) / 1024 * 1024;
   }
-  __host__ __device__ static int warp_bytes(int w) { return 2 * stage_bytes(w) + 4 * AGG * (int)sizeof(T); }
-  __host__ __device__ static size_t cta_bytes(int w) { return 1024 + (size_t)kStreamWarps * warp_bytes(w); }
+  __host__ __device__ static int warp_bytes(int w, int ns) { return ns * stage_bytes(w) + 4 * AGG * (int)sizeof(T); }
+  __host__ __device__ static size_t cta_bytes(int w, int ns) { return 1024 + (size_t)kStreamWarps * warp_bytes(w, ns); }
 };
 
 struct StreamArgs {
@@ -128,13 +128,22 @@ struct StreamArgs {
   int qp, rp, V;       // gap geometry of block B = E*G (k1d_medium.cuh MedGeom)
   int chunk_vec;       // chunk rows are 16-B aligned (else staged element-wise)
   int stage_bytes, warp_bytes;
+  int nstages;         // staging ring per warp: 2..4 (nstages-1 segments in flight)
 };
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+// wait until at most n-1 copy groups are pending (n = 2..4, warp-uniform)
+__device__ __forceinline__ void cp_async_wait_ring(int n) {
+  if (n >= 4)
+    asm volatile("cp.async.wait_group 3;" ::: "memory");
+  else if (n == 3)
+    asm volatile("cp.async.wait_group 2;" ::: "memory");
+  else
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+}
 
 // Stage V'[j0, j0 + len) of `row` into the swizzled buffer X (logical index
 // i = V' index - j0).  j0 and hld are multiples of VEC, so every 16-B unit
@@ -215,23 +224,32 @@ __global__ void __launch_bounds__(32 * kStreamWarps) k_stream_fused(StreamArgs a
     }
   };
 
-  if (gw < a.nseg) {
-    int64_t row, j0;
-    seg_pos(gw, row, j0);
-    stream_stage<T>(a, stg(0), row, j0, seg_len(j0), lane);
-  }
-  cp_async_commit();
-  int it = 0;
-  for (int64_t sg = gw; sg < a.nseg; sg += nw, ++it) {
-    if (sg + nw < a.nseg) {  // the next segment's copy flies while this one computes
+  const int ns = a.nstages;
+  for (int k = 0; k + 1 < ns; ++k) {  // prologue: the first ns-1 segments in flight
+    const int64_t sg = gw + k * nw;
+    if (sg < a.nseg) {
       int64_t row, j0;
-      seg_pos(sg + nw, row, j0);
-      stream_stage<T>(a, stg((it + 1) & 1), row, j0, seg_len(j0), lane);
+      seg_pos(sg, row, j0);
+      stream_stage<T>(a, stg(k), row, j0, seg_len(j0), lane);
     }
     cp_async_commit();
-    cp_async_wait1();
+  }
+  int it = 0, slot = 0;
+  for (int64_t sg = gw; sg < a.nseg; sg += nw, ++it) {
+    {  // keep ns-1 segments in flight
+      const int64_t nx = sg + (ns - 1) * nw;
+      if (nx < a.nseg) {
+        int64_t row, j0;
+        seg_pos(nx, row, j0);
+        const int sl = slot + ns - 1 < ns ? slot + ns - 1 : slot - 1;
+        stream_stage<T>(a, stg(sl), row, j0, seg_len(j0), lane);
+      }
+    }
+    cp_async_commit();
+    cp_async_wait_ring(ns);
     __syncwarp();
-    const unsigned char *X = stg(it & 1);
+    const unsigned char *X = stg(slot);
+    slot = slot + 1 < ns ? slot + 1 : 0;
     int64_t row, j0;
     seg_pos(sg, row, j0);
     const int64_t left = a.c - j0;
@@ -373,7 +391,7 @@ __global__ void __launch_bounds__(32 * kStreamWarps) k_stream_fused(StreamArgs a
         *reinterpret_cast<uint4 *>(ho + t) = u4;
       }
     }
-    __syncwarp();  // X is restaged two segments later; the aggregates next segment
+    __syncwarp();  // X is restaged by the next iteration; the aggregates too
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
@@ -407,8 +425,23 @@ StreamLayout stream_layout(int64_t streams, int64_t w, int64_t max_chunk) {
 }
 
 template <typename T, int G>
-int launch_fused_g(const StreamArgs &a, cudaStream_t s) {
-  const size_t smem = StreamGeo<T>::cta_bytes(a.w);
+int launch_fused_g(StreamArgs a, cudaStream_t s) {
+  // staging depth: the most segments in flight per SM (3 CTAs fit the registers)
+  int best = 2;
+  {
+    int64_t best_fly = -1;
+    for (int ns = 2; ns <= 4; ++ns) {
+      const int64_t ctas = std::min<int64_t>(3, (int64_t)(220 * 1024) / (int64_t)StreamGeo<T>::cta_bytes(a.w, ns));
+      const int64_t fly = ctas * kStreamWarps * (ns - 1);
+      if (fly > best_fly) {
+        best_fly = fly;
+        best = ns;
+      }
+    }
+  }
+  a.nstages = best;
+  a.warp_bytes = StreamGeo<T>::warp_bytes(a.w, best);
+  const size_t smem = StreamGeo<T>::cta_bytes(a.w, best);
   static int attr_set = 0;  // the largest dynamic smem size this instantiation was opened to
   if ((int)smem > attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_stream_fused<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -461,7 +494,6 @@ int launch_stream_push(void *state, const StreamLayout &L, int64_t streams, int6
     if (a.V + 32 / G > Geo::AGG) return kErrUnsupported;
     a.chunk_vec = (reinterpret_cast<uintptr_t>(chunk) % 16 == 0 && (chunk_ld * (int64_t)sizeof(T)) % 16 == 0) ? 1 : 0;
     a.stage_bytes = Geo::stage_bytes((int)w);
-    a.warp_bytes = Geo::warp_bytes((int)w);
     switch (G) {
       case 1: return launch_fused_g<T, 1>(a, s);
       case 2: return launch_fused_g<T, 2>(a, s);

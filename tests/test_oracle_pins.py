@@ -478,3 +478,77 @@ def test_stream_comparison_and_wedge_bounds(family):
         if family in ("increasing", "decreasing"):
             assert st.comparisons <= 2 * n
         assert st.peak_wedge <= w + 1
+
+
+# ---------------------------------------------------------------- N4 morphology
+def test_morph_exhaustive_brute_equals_composition():
+    """Every {0,1,2}^n, n <= 7, every w <= n: the definition (R20) = the composition."""
+    for n in range(1, 8):
+        for a in itertools.product(range(3), repeat=n):
+            a = np.array(a, np.int16)
+            for w in range(1, n + 1):
+                bo, bc = oracle.morph(a, w, brute=True)
+                co, cc = oracle.morph(a, w)
+                assert same(bo, co) and same(bc, cc), (a, w)
+
+
+def test_morph_hand_examples():
+    """Opening removes peaks narrower than w and keeps plateaus of width >= w; closing
+    fills narrow valleys (worked by hand)."""
+    a = np.array([0, 0, 5, 0, 0, 7, 7, 7, 0, 0], np.int32)
+    op, cl = oracle.morph(a, 3, brute=True)
+    assert op.tolist() == [0, 0, 0, 0, 0, 7, 7, 7, 0, 0]
+    assert cl.tolist() == [5, 5, 5, 5, 5, 7, 7, 7, 7, 7]  # windows stay inside: the ends are filled too
+    b = np.array([4, 4, 1, 4, 4, 4], np.int32)
+    op, cl = oracle.morph(b, 2, brute=True)
+    assert cl.tolist() == [4, 4, 4, 4, 4, 4]  # the width-1 valley is filled
+    assert op.tolist() == [4, 4, 1, 4, 4, 4]
+
+
+@pytest.mark.parametrize("dtype", oracle.DTYPES)
+def test_morph_properties_and_scipy(dtype):
+    """Anti-extensive opening, extensive closing, idempotence, and scipy.ndimage
+    grey_opening / grey_closing away from the borders (the operators are translation
+    invariant, so the origin convention cancels in the interior)."""
+    from scipy import ndimage
+
+    a = synth.random_values(np.dtype(dtype), 4000, seed=21)
+    for w in (1, 2, 5, 16, 33):
+        op, cl = oracle.morph(a, w)
+        assert np.all(op <= a) and np.all(cl >= a)
+        op2, _ = oracle.morph(op, w)
+        _, cl2 = oracle.morph(cl, w)
+        assert same(op2, op) and same(cl2, cl)
+        if np.dtype(dtype).itemsize == 8 and np.dtype(dtype).kind in "iu":
+            continue  # scipy.ndimage computes 64-bit integers through float64
+        so = ndimage.grey_opening(a, size=w)
+        sc = ndimage.grey_closing(a, size=w)
+        lo, hi = 2 * w, a.shape[0] - 2 * w
+        assert same(op[lo:hi], so[lo:hi]) and same(cl[lo:hi], sc[lo:hi])
+
+
+def test_morph_duality_f64():
+    a = synth.random_values(np.dtype(np.float64), 3000, seed=4)
+    for w in (3, 40):
+        op, cl = oracle.morph(a, w)
+        nop, ncl = oracle.morph(-a, w)
+        assert same(cl, -nop) and same(op, -ncl)
+
+
+def test_morph_2d_brute_and_scipy():
+    from scipy import ndimage
+
+    rng = np.random.default_rng(9)
+    for (rows, cols, wr, wc) in [(5, 6, 2, 3), (7, 7, 3, 3), (4, 9, 4, 1), (6, 5, 1, 2), (8, 8, 8, 8)]:
+        a = rng.integers(0, 4, size=(2, rows, cols)).astype(np.uint8)
+        bo, bc = oracle.morph_2d(a, wr, wc, brute=True)
+        co, cc = oracle.morph_2d(a, wr, wc)
+        assert same(bo, co) and same(bc, cc), (rows, cols, wr, wc)
+    a = synth.random_values(np.dtype(np.uint8), 120 * 130, seed=3).reshape(120, 130)
+    op, cl = oracle.morph_2d(a, 5, 7)
+    so = ndimage.grey_opening(a, size=(7, 5))
+    sc = ndimage.grey_closing(a, size=(7, 5))
+    assert same(op[14:-14, 10:-10], so[14:-14, 10:-10]) and same(cl[14:-14, 10:-10], sc[14:-14, 10:-10])
+    r1o, r1c = oracle.morph(a[3], 5)  # one row, w_col = 1: the 1-D operators
+    o1, c1 = oracle.morph_2d(a[3:4], 5, 1)
+    assert same(o1[0], r1o) and same(c1[0], r1c)
