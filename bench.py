@@ -199,7 +199,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS) + ["C1", "C3", "C4", "N1", "N2", "N3"])
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS) + ["C1", "C3", "C4", "N1", "N2", "N3", "N4"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -222,7 +222,7 @@ def main():
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if args.config in ("C1", "C3", "C4", "N1", "N2", "N3"):
+    if args.config in ("C1", "C3", "C4", "N1", "N2", "N3", "N4"):
         from bench_extra import run_extra
 
         return run_extra(args, rank, world, local)

@@ -1,4 +1,4 @@
-"""bench.py --config C1|C3|C4|N1|N2|N3: the other BASELINE.json workloads (item-sharded,
+"""bench.py --config C1|C3|C4|N1|N2|N3|N4: the other BASELINE.json workloads (item-sharded,
 no communication) and the NEXT rows of SURVEY.md §8(f) built so far.  Same JSON
 line schema as bench.py; imported by bench.py."""
 from __future__ import annotations
@@ -271,6 +271,38 @@ def run_extra(args, rank, world, local):
         e2e = {"value": outs / (ems / max(1, steps // 2) / 1e3), "unit": bench.UNIT,
                "h2d_bytes_per_step": 4 * rows * n, "d2h_bytes_per_step": 8 * rows * n,
                "path": "MaxMinStream.push per 256-sample chunk from pinned host, outputs back per push"}
+    elif cfg == "N4":
+        # SURVEY.md §8(f) N4 on C3's series: grayscale opening and closing, w = 129,
+        # one fused pass (input read once, both outputs written once)
+        B, n, w = synth.C3["batch"], synth.C3["n"], synth.C3["w"]
+        r0, r1 = shard.shard_items(B, world, rank)
+        rows = r1 - r0
+        host = torch.empty(rows, n, dtype=torch.float32).pin_memory()
+        synth.c3(rows=rows, row0=r0, out=host.numpy())
+        x = host.to(dev)
+        oo = torch.empty(rows, n, dtype=torch.float32, device=dev)
+        oc = torch.empty_like(oo)
+
+        def step():
+            mm.maxmin_morph_batched(x, w, out_open=oo, out_close=oc)
+
+        nb = 4 * rows * n * 3
+        outs = 2 * B * n
+        steps = args.steps
+        name = "N4: grayscale opening + closing of 65536 fp32 series x 4096 (C3), w=129, sharded by series"
+        dtype = "f32"
+        l2 = "inputs (1 GiB) larger than the 126 MB L2"
+        step()
+        torch.cuda.synchronize()
+        import oracle
+
+        parity = True
+        for b in range(0, rows, max(1, rows // 128)):
+            eo, ec = oracle.morph(host[b].numpy(), w)
+            parity = parity and bool(np.array_equal(oo[b].cpu().numpy(), eo) and np.array_equal(oc[b].cpu().numpy(), ec))
+        ms, clk = _timed(step, steps, args.warmup, world, dev)
+        sample = None
+        windows = (w,)
     else:
         raise SystemExit(f"unknown config {cfg}")
 

@@ -234,6 +234,37 @@ int maxmin_stream_push(maxmin_stream *st, const void *chunk, int64_t c, int64_t 
                        void *stream);
 
 /*
+ * Grayscale opening and closing (the image-processing use
+ * of the filter: erosion = the min filter, dilation = the max
+ * filter).  The flat structuring element (w samples; a w_col x w_row
+ * rectangle in 2-D) stays inside the data (reading R20):
+ *   open[i]  = max, over the windows inside the row that contain i, of their min
+ *   close[i] = min, over the same windows, of their max
+ * for EVERY position i: outputs have the input's shape.
+ *
+ * maxmin_morph_batched: rows b of in + b*in_ld (n samples each); out_open /
+ *   out_close (either may be NULL) rows at pitch out_ld, 16-byte aligned with
+ *   16-byte row pitch; in needs element alignment.  w - 1 <= 1024 (else
+ *   MAXMIN_ERR_UNSUPPORTED).  One fused kernel: the input is read once and
+ *   each output written once.  No workspace.
+ * maxmin_morph_2d: images as maxmin_filter_2d; outputs [batch][rows][cols]
+ *   with pitch out_ld / out_bstride, element alignment.  Device workspace of
+ *   maxmin_morph_2d_workspace_bytes (two padded copies of the image: the
+ *   erosion and the dilation framed by the identities).  Runs as the 2-D
+ *   filter, then its max over the padded erosion and min over the padded
+ *   dilation (the rectangle opening is not separable into 1-D openings).
+ */
+int maxmin_morph_batched(int dt, const void *in, int64_t batch, int64_t n, int64_t in_ld,
+                         int64_t w, void *out_open, void *out_close, int64_t out_ld,
+                         void *stream);
+int maxmin_morph_2d_workspace_bytes(int dt, int64_t batch, int64_t rows, int64_t cols,
+                                    int64_t w_row, int64_t w_col, size_t *bytes);
+int maxmin_morph_2d(int dt, const void *in, int64_t batch, int64_t rows, int64_t cols,
+                    int64_t in_ld, int64_t in_bstride, int64_t w_row, int64_t w_col,
+                    void *out_open, void *out_close, int64_t out_ld, int64_t out_bstride,
+                    void *workspace, size_t workspace_bytes, void *stream);
+
+/*
  * End-to-end 1-D call on HOST buffers (in, out_max, out_min are host
  * pointers; page-locked memory gives full PCIe bandwidth).  The input is
  * streamed to the device in chunks (with a (w-1)-element overlap), filtered

@@ -20,7 +20,8 @@ __all__ = [
     "MaxMinError", "dtype_code", "maxmin_workspace_bytes", "maxmin_filter_1d",
     "maxmin_filter_batched", "maxmin_filter_2d", "maxmin_filter_1d_host",
     "maxmin_host_workspace_bytes", "maxmin_argfilter_workspace_bytes", "maxmin_argfilter_batched",
-    "maxmin_argfilter_1d", "maxmin_lb_keogh_batched", "maxmin_stream_state_bytes", "MaxMinStream", "version",
+    "maxmin_argfilter_1d", "maxmin_lb_keogh_batched", "maxmin_stream_state_bytes", "MaxMinStream", "maxmin_morph_batched",
+    "maxmin_morph_1d", "maxmin_morph_2d", "version",
 ]
 
 _CODES = {
@@ -255,6 +256,66 @@ class MaxMinStream:
             ctypes.byref(self._st), _ptr(chunk), c, chunk.stride(0), _ptr(out_max), _ptr(out_min), out_ld,
             ctypes.byref(fv), _stream_ptr(stream)))
         return out_max, out_min, int(fv.value)
+
+
+def maxmin_morph_batched(x: torch.Tensor, w: int, n: int | None = None, out_open=None, out_close=None, *,
+                         want_open=True, want_close=True, stream=None):
+    """Grayscale opening and closing (N4) of every row of a 2-D CUDA tensor [batch, ld] (first
+    n columns) by a flat segment of w samples; returns (open, close), each [batch, n]."""
+    if x.dim() != 2 or not x.is_cuda or x.stride(1) != 1:
+        raise ValueError("maxmin_morph_batched: x must be a row-major 2-D CUDA tensor")
+    batch, ncols = x.shape
+    n = ncols if n is None else n
+    vec = max(16 // x.element_size(), 1)
+    n_pad = (n + vec - 1) // vec * vec
+    if want_open and out_open is None:
+        out_open = torch.empty(batch, n_pad, dtype=x.dtype, device=x.device)[:, :n]
+    if want_close and out_close is None:
+        out_close = torch.empty(batch, n_pad, dtype=x.dtype, device=x.device)[:, :n]
+    o = out_open if out_open is not None else out_close
+    _lib.check(_lib.lib().maxmin_morph_batched(dtype_code(x.dtype), _ptr(x), batch, n, x.stride(0), w,
+                                               _ptr(out_open), _ptr(out_close), o.stride(0) if o is not None else n,
+                                               _stream_ptr(stream)))
+    return out_open, out_close
+
+
+def maxmin_morph_1d(x: torch.Tensor, w: int, **kw):
+    """Opening and closing of a contiguous 1-D CUDA tensor (see maxmin_morph_batched)."""
+    if x.dim() != 1 or not x.is_cuda or not x.is_contiguous():
+        raise ValueError("maxmin_morph_1d: x must be a contiguous 1-D CUDA tensor")
+    op, cl = maxmin_morph_batched(x[None], w, **kw)
+    return (op[0] if op is not None else None), (cl[0] if cl is not None else None)
+
+
+def maxmin_morph_2d(x: torch.Tensor, w_row: int, w_col: int, cols: int | None = None, out_open=None,
+                    out_close=None, *, want_open=True, want_close=True, workspace=None, stream=None):
+    """Opening and closing (N4) of [batch, rows, ld] (or [rows, ld]) images by a flat
+    w_col x w_row rectangle; outputs have the images' shape."""
+    squeeze = x.dim() == 2
+    xx = x[None] if squeeze else x
+    if xx.dim() != 3 or not xx.is_cuda or xx.stride(2) != 1:
+        raise ValueError("maxmin_morph_2d: x must be a row-major [batch, rows, ld] CUDA tensor")
+    batch, rows, ld = xx.shape
+    cols = ld if cols is None else cols
+    if want_open and out_open is None:
+        out_open = torch.empty(batch, rows, cols, dtype=x.dtype, device=x.device)
+    if want_close and out_close is None:
+        out_close = torch.empty(batch, rows, cols, dtype=x.dtype, device=x.device)
+    o = out_open if out_open is not None else out_close
+    if o is not None and o.dim() == 2:
+        o = o[None]
+    need = ctypes.c_size_t(0)
+    _lib.check(_lib.lib().maxmin_morph_2d_workspace_bytes(dtype_code(x.dtype), batch, rows, cols, w_row, w_col,
+                                                          ctypes.byref(need)))
+    if workspace is None:
+        workspace = torch.empty(max(need.value, 16), dtype=torch.uint8, device=x.device)
+    _lib.check(_lib.lib().maxmin_morph_2d(
+        dtype_code(x.dtype), _ptr(xx), batch, rows, cols, xx.stride(1), xx.stride(0), w_row, w_col, _ptr(out_open),
+        _ptr(out_close), o.stride(1), o.stride(0), _ptr(workspace), workspace.numel(), _stream_ptr(stream)))
+    if squeeze:
+        out_open = out_open[0] if out_open is not None and out_open.dim() == 3 else out_open
+        out_close = out_close[0] if out_close is not None and out_close.dim() == 3 else out_close
+    return out_open, out_close
 
 
 def maxmin_host_workspace_bytes(dtype, n: int, w: int, chunk: int = 0) -> int:

@@ -65,6 +65,11 @@ SIGNATURES = {
     "maxmin_stream_state_bytes": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i64, ctypes.POINTER(_sz)]),
     "maxmin_stream_init": (ctypes.c_int, [_sp, ctypes.c_int, _i64, _i64, _i64, _vp, _sz, _vp]),
     "maxmin_stream_push": (ctypes.c_int, [_sp, _vp, _i64, _i64, _vp, _vp, _i64, ctypes.POINTER(_i64), _vp]),
+    "maxmin_morph_batched": (ctypes.c_int, [ctypes.c_int, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp]),
+    "maxmin_morph_2d_workspace_bytes": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i64, _i64, _i64,
+                                                       ctypes.POINTER(_sz)]),
+    "maxmin_morph_2d": (ctypes.c_int, [ctypes.c_int, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp,
+                                       _i64, _i64, _vp, _sz, _vp]),
     "maxmin_host_workspace_bytes": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i64, ctypes.POINTER(_sz)]),
     "maxmin_filter_1d_host": (ctypes.c_int, [ctypes.c_int, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _sz]),
 }

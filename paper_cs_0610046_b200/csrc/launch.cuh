@@ -48,6 +48,16 @@ StreamLayout stream_layout(int64_t streams, int64_t w, int64_t max_chunk);
 template <typename T>
 int launch_stream_push(void *state, const StreamLayout &L, int64_t streams, int64_t w, int phase, const T *chunk,
                        int64_t c, int64_t chunk_ld, T *out_max, T *out_min, int64_t out_ld, cudaStream_t s);
+// grayscale opening / closing (morph.cu)
+template <typename T>
+int launch_morph(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w, void *out_open,
+                 void *out_close, int64_t out_ld, cudaStream_t s);
+template <typename T>
+size_t morph_2d_workspace(int64_t batch, int64_t rows, int64_t cols, int64_t w_row, int64_t w_col);
+template <typename T>
+int launch_morph_2d(const void *in, int64_t batch, int64_t rows, int64_t cols, int64_t in_ld, int64_t in_bstride,
+                    int64_t w_row, int64_t w_col, void *out_open, void *out_close, int64_t out_ld,
+                    int64_t out_bstride, void *ws, cudaStream_t s);
 int encode_u8_map(CUtensorMap *map, const void *base, const int64_t dims[3], const int64_t strides[2],
                   const int box[3]);  // maxmin_abi.cu
 int encode_rows_map(CUtensorMap *map, const void *in, int elem_bytes, int64_t rows_per_series,

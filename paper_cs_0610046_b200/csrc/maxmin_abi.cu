@@ -483,6 +483,82 @@ int maxmin_stream_push(maxmin_stream *st, const void *chunk, int64_t c, int64_t 
   return rc;
 }
 
+// ------------------------------------------------------------ N4: morphology
+int maxmin_morph_batched(int dt, const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w,
+                         void *out_open, void *out_close, int64_t out_ld, void *stream) {
+  const size_t sz = maxmin_dtype_size(dt);
+  if (!sz) return MAXMIN_ERR_DTYPE;
+  if (!in || (!out_open && !out_close)) return MAXMIN_ERR_NULL;
+  if (w < 1) return MAXMIN_ERR_WINDOW;
+  if (n < 1 || batch < 0) return MAXMIN_ERR_SHAPE;
+  if (w > n) return MAXMIN_ERR_WINDOW_TOO_LARGE;
+  if (w - 1 > 1024) return MAXMIN_ERR_UNSUPPORTED;
+  if (in_ld < n || out_ld < n) return MAXMIN_ERR_SHAPE;
+  size_t ib, ob;
+  if (!extent(batch, n, in_ld, sz, &ib) || !extent(batch, n, out_ld, sz, &ob)) return MAXMIN_ERR_SHAPE;
+  if ((reinterpret_cast<uintptr_t>(in) % sz) != 0) return MAXMIN_ERR_ALIGNMENT;
+  if ((out_open && !aligned16(out_open)) || (out_close && !aligned16(out_close))) return MAXMIN_ERR_ALIGNMENT;
+  if (batch > 1 && ((size_t)out_ld * sz) % 16 != 0) return MAXMIN_ERR_ALIGNMENT;
+  if (batch == 0) return MAXMIN_OK;
+  if (out_open && overlap(in, ib, out_open, ob)) return MAXMIN_ERR_ALIAS;
+  if (out_close && overlap(in, ib, out_close, ob)) return MAXMIN_ERR_ALIAS;
+  if (out_open && out_close && overlap(out_open, ob, out_close, ob)) return MAXMIN_ERR_ALIAS;
+  int rc;
+  if ((rc = ensure_device(in)) != MAXMIN_OK) return rc;
+  if (out_open && (rc = ensure_device(out_open)) != MAXMIN_OK) return rc;
+  if (out_close && (rc = ensure_device(out_close)) != MAXMIN_OK) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  MM_DISPATCH(dt, return mm::launch_morph<T>(in, batch, n, in_ld, w, out_open, out_close, out_ld, s))
+}
+
+int maxmin_morph_2d_workspace_bytes(int dt, int64_t batch, int64_t rows, int64_t cols, int64_t w_row,
+                                    int64_t w_col, size_t *bytes) {
+  if (!bytes) return MAXMIN_ERR_NULL;
+  *bytes = 0;
+  if (!maxmin_dtype_size(dt)) return MAXMIN_ERR_DTYPE;
+  if (w_row < 1 || w_col < 1) return MAXMIN_ERR_WINDOW;
+  if (batch < 0 || rows < 1 || cols < 1) return MAXMIN_ERR_SHAPE;
+  if (w_row > cols || w_col > rows) return MAXMIN_ERR_WINDOW_TOO_LARGE;
+  size_t t;
+  if (!extent(batch, (rows + w_col) * (cols + w_row + 16), (rows + w_col) * (cols + w_row + 16), 8, &t))
+    return MAXMIN_ERR_SHAPE;
+  MM_DISPATCH(dt, { *bytes = mm::morph_2d_workspace<T>(batch, rows, cols, w_row, w_col); return MAXMIN_OK; })
+}
+
+int maxmin_morph_2d(int dt, const void *in, int64_t batch, int64_t rows, int64_t cols, int64_t in_ld,
+                    int64_t in_bstride, int64_t w_row, int64_t w_col, void *out_open, void *out_close,
+                    int64_t out_ld, int64_t out_bstride, void *workspace, size_t workspace_bytes, void *stream) {
+  const size_t sz = maxmin_dtype_size(dt);
+  if (!sz) return MAXMIN_ERR_DTYPE;
+  if (!in || (!out_open && !out_close)) return MAXMIN_ERR_NULL;
+  size_t need = 0;
+  int rc = maxmin_morph_2d_workspace_bytes(dt, batch, rows, cols, w_row, w_col, &need);
+  if (rc != MAXMIN_OK) return rc;
+  if (in_ld < cols || out_ld < cols) return MAXMIN_ERR_SHAPE;
+  if (batch > 1 && (in_bstride < rows * in_ld || out_bstride < rows * out_ld)) return MAXMIN_ERR_SHAPE;
+  size_t ib, ob, t1, t2;
+  if (!extent(rows, cols, in_ld, sz, &t1) || !extent(rows, cols, out_ld, sz, &t2)) return MAXMIN_ERR_SHAPE;
+  if (!extent(batch, (int64_t)(t1 / sz), batch > 1 ? in_bstride : 0, sz, &ib) ||
+      !extent(batch, (int64_t)(t2 / sz), batch > 1 ? out_bstride : 0, sz, &ob))
+    return MAXMIN_ERR_SHAPE;
+  auto el = [sz](const void *p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) % sz) == 0; };
+  if (!el(in) || !el(out_open) || !el(out_close)) return MAXMIN_ERR_ALIGNMENT;
+  if (!workspace || workspace_bytes < need || !aligned16(workspace)) return MAXMIN_ERR_WORKSPACE;
+  if (batch == 0) return MAXMIN_OK;
+  const void *regs[4] = {in, out_open, out_close, workspace};
+  const size_t rb[4] = {ib, ob, ob, need};
+  for (int i = 0; i < 4; ++i)
+    for (int k = i + 1; k < 4; ++k)
+      if (regs[i] && regs[k] && overlap(regs[i], rb[i], regs[k], rb[k])) return MAXMIN_ERR_ALIAS;
+  if ((rc = ensure_device(in)) != MAXMIN_OK) return rc;
+  if (out_open && (rc = ensure_device(out_open)) != MAXMIN_OK) return rc;
+  if (out_close && (rc = ensure_device(out_close)) != MAXMIN_OK) return rc;
+  if ((rc = ensure_device(workspace)) != MAXMIN_OK) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  MM_DISPATCH(dt, return mm::launch_morph_2d<T>(in, batch, rows, cols, in_ld, in_bstride, w_row, w_col, out_open,
+                                                out_close, out_ld, out_bstride, workspace, s))
+}
+
 // ------------------------------------------------------------ host pipeline
 static int64_t default_chunk(int64_t chunk) { return chunk > 0 ? chunk : (int64_t(1) << 24); }
 

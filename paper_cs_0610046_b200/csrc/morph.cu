@@ -1,0 +1,408 @@
+// morph.cu -- grayscale opening and closing.
+//
+// The 2-D application family of the filter: "applied to images ... by first
+// applying the unidimensional on rows and then on columns";
+// erosion is the min filter, dilation the max filter, and the opening /
+// closing are their compositions.  With the structuring element kept inside
+// the data (reading R20), for every position i of a row of n:
+//   e[j] = min a[j .. j+w),  d[j] = max a[j .. j+w)          j in [0, m), m = n-w+1
+//   open[i]  = max e[j] over j in [i-w+1, i] ∩ [0, m)
+//   close[i] = min d[j] over the same j
+//
+// 1-D / batched rows (k_morph_fused): ONE pass -- the input is read once, the
+// opening and the closing are written once each.  Warp-autonomous like the
+// fused stream push (stream.cu): a warp owns a segment of 32E outputs of one
+// row, stages a[j0-(w-1), j0+32E+w-1) with cp.async into its swizzled buffer
+// (a ring of segments in flight), computes e and d for the 32E+w-1 positions
+// [j0-(w-1), j0+32E) into two on-chip buffers (positions outside [0, m) get
+// the identity of the next step: lowest for e, highest for d), then the max
+// over e and the min over d (kwarp.cuh: near/far blocks for w-1 >= E,
+// log-step + barrel shift for w <= E).  w-1 <= kMorphHMax.
+//
+// 2-D images (launch_morph_2d): the rectangle opening is not a product of 1-D
+// openings (max and min along different axes do not commute), so it runs as a
+// composition of the library's 2-D filter: e and d of the valid region into
+// the interior of two padded buffers whose (w-1)-wide frames hold the
+// identities, then the 2-D max over the padded e and the 2-D min over the
+// padded d.  HBM: 1 read + 2 writes + 2 reads + 2 writes (vs 1 + 2 fused).
+#include "kwarp.cuh"
+#include "launch.cuh"
+
+#include <limits>
+
+namespace mm {
+
+constexpr int kMorphWarps = 4;
+constexpr int kMorphHMax = 1024;  // largest w-1 of k_morph_fused
+
+template <typename T>
+__device__ __forceinline__ T lowest_value() {
+  if constexpr (std::is_floating_point<T>::value) return -std::numeric_limits<T>::infinity();
+  else return std::numeric_limits<T>::lowest();
+}
+template <typename T>
+__device__ __forceinline__ T highest_value() {
+  if constexpr (std::is_floating_point<T>::value) return std::numeric_limits<T>::infinity();
+  else return std::numeric_limits<T>::max();
+}
+
+template <typename T>
+struct MorphGeo {
+  // 8 elements per lane (16 for bytes: one 16-B unit): ~100 registers, more warps in flight
+  static constexpr int E = sizeof(T) == 1 ? 16 : 8;
+  static constexpr int VEC = 16 / (int)sizeof(T);
+  static constexpr int SEG = 32 * E;
+  __host__ __device__ static int round1k(int bytes) { return (bytes + 127) / 128 * 128; }  // 128-B rows
+  // staged input: P1 + (rounds of pass 1) + w - 1 + over-reads
+  __host__ __device__ static int stage_bytes(int w) { return round1k((3 * VEC + 2 * SEG + 2 * w + 2 * E) * (int)sizeof(T)); }
+  // e / d buffers: rounds of pass 1 (<= 2*SEG + w) + pass-2 over-reads
+  __host__ __device__ static int ebuf_bytes(int w) { return round1k((2 * SEG + w + 2 * E + 2 * VEC) * (int)sizeof(T)); }
+  __host__ __device__ static int warp_bytes(int w, int ns) {
+    return ns * stage_bytes(w) + 2 * ebuf_bytes(w) + WarpAgg<T>::bytes();
+  }
+  __host__ __device__ static size_t cta_bytes(int w, int ns, int warps = kMorphWarps) {
+    return 1024 + (size_t)warps * warp_bytes(w, ns);
+  }
+};
+
+struct MorphArgs {
+  const void *in;
+  void *out_open;
+  void *out_close;
+  int64_t n, m, in_ld, out_ld, batch;
+  int64_t segs_per_row, nseg;
+  WarpGeom g;
+  int w;
+  int in_vec;  // input rows 16-B aligned
+  int stage_bytes, ebuf_bytes, warp_bytes, nstages;
+};
+
+__device__ __forceinline__ void mcp_async16(void *smem, const void *g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void mcp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void mcp_async_wait_ring(int n) {
+  if (n >= 4)
+    asm volatile("cp.async.wait_group 3;" ::: "memory");
+  else if (n == 3)
+    asm volatile("cp.async.wait_group 2;" ::: "memory");
+  else
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+}
+
+// first staged position of segment j0 (16-B aligned, may be negative) and the
+// offset P1 of a[j0-(w-1)] in the staged buffer
+__device__ __forceinline__ void morph_base(int64_t j0, int w, int vec, int64_t &a0, int &p1) {
+  const int64_t s = j0 - (w - 1);
+  p1 = (int)(((s % vec) + vec) % vec);
+  a0 = s - p1;
+}
+
+template <typename T>
+__device__ __forceinline__ void morph_stage(const MorphArgs &a, unsigned char *X, int64_t row, int64_t j0, int lane) {
+  constexpr int VEC = 16 / (int)sizeof(T);
+  constexpr int SEG = MorphGeo<T>::SEG;
+  int64_t a0;
+  int p1;
+  morph_base(j0, a.w, VEC, a0, p1);
+  const int64_t want_end = j0 + SEG + a.w - 1;  // exclusive
+  const int64_t end = want_end < a.n ? want_end : a.n;
+  const int nq = (int)((end - a0 + VEC - 1) / VEC);
+  const T *src = static_cast<const T *>(a.in) + row * a.in_ld;
+  for (int q = lane; q < nq; q += 32) {
+    const int64_t v = a0 + (int64_t)q * VEC;
+    unsigned char *dst = X + swz(q);
+    if (a.in_vec && v >= 0 && v + VEC <= a.n) {
+      mcp_async16(dst, src + v);
+    } else {
+      T t[VEC];
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) {
+        const int64_t u = v + k;
+        t[k] = (u >= 0 && u < a.n) ? src[u] : T(0);
+      }
+      uint4 u4;
+      memcpy(&u4, t, 16);
+      *reinterpret_cast<uint4 *>(dst) = u4;
+    }
+  }
+}
+
+// E elements at logical position pos (a multiple of E) of a swizzled buffer
+template <typename T, int E>
+__device__ __forceinline__ void sts_swz_chunk(unsigned char *buf, int pos, const T (&v)[E]) {
+  constexpr int VEC = 16 / (int)sizeof(T);
+  static_assert((E % VEC) == 0, "whole 16-B units");
+#pragma unroll
+  for (int u = 0; u < E / VEC; ++u) {
+    uint4 q;
+    memcpy(&q, &v[u * VEC], 16);
+    *reinterpret_cast<uint4 *>(buf + swz(pos / VEC + u)) = q;
+  }
+}
+
+template <typename T, int E, int G, bool TWO>
+__device__ __forceinline__ void morph_window(const unsigned char *XA, const unsigned char *XB, int pos0,
+                                             const WarpGeom &g, const WarpAgg<T> &agg, int lane, T (&ox)[E],
+                                             T (&on)[E]) {
+  if constexpr (G == 0)
+    warp_window_small<T, E, TWO>(XA, XB, pos0, g.w, lane, ox, on);
+  else
+    warp_window_med<T, E, G, TWO>(XA, XB, pos0, g, agg, lane, ox, on);
+}
+
+template <typename T, int G>
+__global__ void __launch_bounds__(32 * kMorphWarps) k_morph_fused(MorphArgs a) {
+  using Geo = MorphGeo<T>;
+  constexpr int E = Geo::E;
+  constexpr int SEG = Geo::SEG;
+  constexpr int VEC = Geo::VEC;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *base = smem_align1024(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char *wb = base + warp * a.warp_bytes;
+  auto stg = [&](int i) { return wb + i * a.stage_bytes; };
+  unsigned char *EB = wb + a.nstages * a.stage_bytes;  // erosion (lowest outside [0, m))
+  unsigned char *DB = EB + a.ebuf_bytes;               // dilation (highest outside)
+  const WarpAgg<T> agg(DB + a.ebuf_bytes);
+  const int w = a.w;
+  const int nwb = blockDim.x >> 5;
+  const int64_t gw = blockIdx.x * (int64_t)nwb + warp, nw = (int64_t)gridDim.x * nwb;
+  const int rounds = (SEG + w - 1 + SEG - 1) / SEG;  // pass 1: SEG + w - 1 positions
+
+  auto seg_pos = [&](int64_t sg, int64_t &row, int64_t &j0) {  // nseg < 2^31 (launcher)
+    const uint32_t r = (uint32_t)sg / (uint32_t)a.segs_per_row;
+    row = r;
+    j0 = ((int64_t)sg - (int64_t)r * a.segs_per_row) * SEG;
+  };
+  const int ns = a.nstages;
+  for (int k = 0; k + 1 < ns; ++k) {
+    const int64_t sg = gw + k * nw;
+    if (sg < a.nseg) {
+      int64_t row, j0;
+      seg_pos(sg, row, j0);
+      morph_stage<T>(a, stg(k), row, j0, lane);
+    }
+    mcp_async_commit();
+  }
+  int slot = 0;
+  for (int64_t sg = gw; sg < a.nseg; sg += nw) {
+    {
+      const int64_t nx = sg + (ns - 1) * nw;
+      if (nx < a.nseg) {
+        int64_t row, j0;
+        seg_pos(nx, row, j0);
+        morph_stage<T>(a, stg(slot + ns - 1 < ns ? slot + ns - 1 : slot - 1), row, j0, lane);
+      }
+    }
+    mcp_async_commit();
+    mcp_async_wait_ring(ns);
+    __syncwarp();
+    const unsigned char *X = stg(slot);
+    slot = slot + 1 < ns ? slot + 1 : 0;
+    int64_t row, j0;
+    seg_pos(sg, row, j0);
+    int64_t a0;
+    int p1;
+    morph_base(j0, w, VEC, a0, p1);
+    // ---- pass 1: d (max) and e (min) at positions j0-(w-1) + [0, rounds*SEG)
+    for (int r = 0; r < rounds; ++r) {
+      T ox[E], on[E];
+      morph_window<T, E, G, false>(X, X, p1 + r * SEG, a.g, agg, lane, ox, on);
+      const int64_t j = j0 - (w - 1) + r * SEG + lane * E;
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        if (j + k < 0 || j + k >= a.m) {
+          ox[k] = highest_value<T>();
+          on[k] = lowest_value<T>();
+        }
+      }
+      sts_swz_chunk<T, E>(DB, r * SEG + lane * E, ox);
+      sts_swz_chunk<T, E>(EB, r * SEG + lane * E, on);
+    }
+    __syncwarp();
+    // ---- pass 2: opening = max over e, closing = min over d
+    {
+      T op[E], cl[E];
+      if constexpr (G == 0) {
+        warp_window_small1<T, E, true>(EB, 0, w, lane, op);
+        warp_window_small1<T, E, false>(DB, 0, w, lane, cl);
+      } else {
+        warp_window_med1<T, E, G, true>(EB, 0, a.g, agg, lane, op);
+        warp_window_med1<T, E, G, false>(DB, 0, a.g, agg, lane, cl);
+      }
+      const int64_t i0 = j0 + lane * E;
+      const int64_t left = a.n - i0;
+      if (left > 0) {
+        T *oo = a.out_open ? static_cast<T *>(a.out_open) + row * a.out_ld + i0 : nullptr;
+        T *oc = a.out_close ? static_cast<T *>(a.out_close) + row * a.out_ld + i0 : nullptr;
+        if (left >= E) {
+          if (oo) store_chunk<T, E>(oo, op);
+          if (oc) store_chunk<T, E>(oc, cl);
+        } else {
+#pragma unroll
+          for (int k = 0; k < E; ++k)
+            if (k < left) {
+              if (oo) oo[k] = op[k];
+              if (oc) oc[k] = cl[k];
+            }
+        }
+      }
+    }
+    __syncwarp();  // EB / DB and X are rewritten by the next segment
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+template <typename T, int G>
+int launch_morph_g(MorphArgs a, cudaStream_t s) {
+  using Geo = MorphGeo<T>;
+  // warps per CTA and staging depth: the most segments in flight per SM
+  int best_ns = 0, best_nw = 0;
+  int64_t best_fly = -1;
+  for (int nwb = kMorphWarps; nwb >= 1; nwb /= 2) {
+    for (int ns = 2; ns <= 4; ++ns) {
+      const size_t bytes = Geo::cta_bytes(a.w, ns, nwb);
+      if (bytes > 227 * 1024) continue;
+      cudaError_t e = cudaFuncSetAttribute(k_morph_fused<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      if (e != cudaSuccess) return note_cuda(e);
+      int per = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_morph_fused<T, G>, 32 * nwb, bytes);
+      if (e != cudaSuccess) return note_cuda(e);
+      const int64_t fly = (int64_t)per * nwb * (ns - 1);
+      if (fly > best_fly) {
+        best_fly = fly;
+        best_ns = ns;
+        best_nw = nwb;
+      }
+    }
+  }
+  if (best_fly <= 0) return kErrUnsupported;
+  a.nstages = best_ns;
+  a.warp_bytes = Geo::warp_bytes(a.w, best_ns);
+  const size_t smem = Geo::cta_bytes(a.w, best_ns, best_nw);
+  cudaError_t e = cudaFuncSetAttribute(k_morph_fused<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return note_cuda(e);
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_morph_fused<T, G>, 32 * best_nw, smem);
+  if (e != cudaSuccess) return note_cuda(e);
+  const int64_t want = (a.nseg + best_nw - 1) / best_nw;
+  const int64_t cap = (int64_t)sm_count() * per_sm;
+  k_morph_fused<T, G><<<(int)(want < cap ? want : cap), 32 * best_nw, smem, s>>>(a);
+  return note_cuda(cudaGetLastError());
+}
+
+template <typename T>
+int launch_morph(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w, void *out_open,
+                 void *out_close, int64_t out_ld, cudaStream_t s) {
+  using Geo = MorphGeo<T>;
+  if (batch == 0) return kOK;
+  if (w - 1 > kMorphHMax) return kErrUnsupported;
+  MorphArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.in = in;
+  a.out_open = out_open;
+  a.out_close = out_close;
+  a.n = n;
+  a.m = n - w + 1;
+  a.in_ld = in_ld;
+  a.out_ld = out_ld;
+  a.batch = batch;
+  a.segs_per_row = (n + Geo::SEG - 1) / Geo::SEG;
+  a.nseg = batch * a.segs_per_row;
+  if (a.nseg > 0x7fffffffLL) return kErrUnsupported;
+  a.w = (int)w;
+  a.in_vec = (reinterpret_cast<uintptr_t>(in) % 16 == 0 && (in_ld * (int64_t)sizeof(T)) % 16 == 0) ? 1 : 0;
+  a.stage_bytes = Geo::stage_bytes((int)w);
+  a.ebuf_bytes = Geo::ebuf_bytes((int)w);
+  if (w - 1 < Geo::E) {
+    a.g.w = (int)w;
+    return launch_morph_g<T, 0>(a, s);
+  }
+  const int G = warp_group<Geo::E>(w);
+  a.g = make_warp_geom<Geo::E>((int)w, G);
+  if (a.g.V + 32 / G > WarpAgg<T>::AGG) return kErrUnsupported;
+  switch (G) {
+    case 1: return launch_morph_g<T, 1>(a, s);
+    case 2: return launch_morph_g<T, 2>(a, s);
+    case 4: return launch_morph_g<T, 4>(a, s);
+    case 8: return launch_morph_g<T, 8>(a, s);
+    case 16: return launch_morph_g<T, 16>(a, s);
+    default: return launch_morph_g<T, 32>(a, s);
+  }
+}
+
+// ------------------------------------------------------------------- 2-D
+template <typename T>
+__global__ void k_morph_frame(T *pe, T *pd, int64_t batch, int64_t PR, int64_t PC, int64_t ld, int64_t bs,
+                              int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
+  // every element of the padded buffers outside rows [r0, r1) x columns [c0, c1)
+  const int64_t total = batch * PR * PC;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t / (PR * PC), rc = t - b * PR * PC, r = rc / PC, c = rc - r * PC;
+    if (r >= r0 && r < r1 && c >= c0 && c < c1) continue;
+    pe[b * bs + r * ld + c] = lowest_value<T>();
+    pd[b * bs + r * ld + c] = highest_value<T>();
+  }
+}
+
+template <typename T>
+size_t morph_2d_workspace(int64_t batch, int64_t rows, int64_t cols, int64_t w_row, int64_t w_col) {
+  constexpr int VEC = 16 / (int)sizeof(T);
+  const int64_t PR = rows + w_col - 1, PC = cols + w_row - 1;
+  const int64_t ld = (PC + VEC - 1) / VEC * VEC;
+  const size_t one = ((size_t)batch * PR * ld * sizeof(T) + 255) & ~size_t(255);
+  return 2 * one;
+}
+
+template <typename T>
+int launch_morph_2d(const void *in, int64_t batch, int64_t rows, int64_t cols, int64_t in_ld, int64_t in_bstride,
+                    int64_t w_row, int64_t w_col, void *out_open, void *out_close, int64_t out_ld,
+                    int64_t out_bstride, void *ws, cudaStream_t s) {
+  constexpr int VEC = 16 / (int)sizeof(T);
+  if (batch == 0) return kOK;
+  const int64_t PR = rows + w_col - 1, PC = cols + w_row - 1;
+  const int64_t ld = (PC + VEC - 1) / VEC * VEC;
+  const int64_t bs = PR * ld;
+  const size_t one = ((size_t)batch * PR * ld * sizeof(T) + 255) & ~size_t(255);
+  T *pe = static_cast<T *>(ws);
+  T *pd = reinterpret_cast<T *>(static_cast<char *>(ws) + one);
+  {
+    const int64_t total = batch * PR * PC;
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 8);
+    k_morph_frame<T><<<(int)(blocks > 0 ? blocks : 1), 256, 0, s>>>(pe, pd, batch, PR, PC, ld, bs, w_col - 1,
+                                                                     w_col - 1 + rows - w_col + 1, w_row - 1,
+                                                                     w_row - 1 + cols - w_row + 1);
+    int rc = note_cuda(cudaGetLastError());
+    if (rc) return rc;
+  }
+  // e (min) and d (max) of the valid region into the frames' interiors
+  const int64_t off = (w_col - 1) * ld + (w_row - 1);
+  int rc = launch_2d<T>(in, batch, rows, cols, in_ld, in_bstride, w_row, w_col, pd + off, pe + off, ld, bs, s);
+  if (rc) return rc;
+  if (out_open) {
+    rc = launch_2d<T>(pe, batch, PR, PC, ld, bs, w_row, w_col, out_open, nullptr, out_ld, out_bstride, s);
+    if (rc) return rc;
+  }
+  if (out_close) rc = launch_2d<T>(pd, batch, PR, PC, ld, bs, w_row, w_col, nullptr, out_close, out_ld, out_bstride, s);
+  return rc;
+}
+
+#define MM_MORPH_INST(T)                                                                                      \
+  template int launch_morph<T>(const void *, int64_t, int64_t, int64_t, int64_t, void *, void *, int64_t,    \
+                               cudaStream_t);                                                                 \
+  template size_t morph_2d_workspace<T>(int64_t, int64_t, int64_t, int64_t, int64_t);                        \
+  template int launch_morph_2d<T>(const void *, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,        \
+                                  int64_t, void *, void *, int64_t, int64_t, void *, cudaStream_t);
+MM_MORPH_INST(uint8_t)
+MM_MORPH_INST(int8_t)
+MM_MORPH_INST(uint16_t)
+MM_MORPH_INST(int16_t)
+MM_MORPH_INST(uint32_t)
+MM_MORPH_INST(int32_t)
+MM_MORPH_INST(uint64_t)
+MM_MORPH_INST(int64_t)
+MM_MORPH_INST(float)
+MM_MORPH_INST(double)
+
+}  // namespace mm

@@ -29,6 +29,7 @@
 //   a push copies the chunk into the slot, runs the batched filter (any 1-D
 //   kernel) over [0, w-1+c) and moves the last w-1 samples to the front.
 //   HBM bytes: 2c + (w-1+c) + 2c + 2(w-1) per stream.
+#include "kwarp.cuh"
 #include "launch.cuh"
 
 namespace mm {
@@ -100,19 +101,18 @@ __global__ void __launch_bounds__(256) k_stream_copy(T *state, int64_t streams, 
 constexpr int kStreamHMax = 1024;  // largest w-1 of the fused kernel
 constexpr int kStreamWarps = 4;    // warps per CTA (~136 registers: 3 CTAs per SM)
 
-template <typename T>
+template <typename T, int E_ = Chunk<T>::E>
 struct StreamGeo {
-  static constexpr int E = Chunk<T>::E;
+  static constexpr int E = E_;
   static constexpr int VEC = 16 / (int)sizeof(T);
   static constexpr int SEG = 32 * E;  // windows per warp segment
-  static constexpr int AGG = 64;      // far-block aggregate slots per warp and kind
   // staged elements: P + SEG + w - 1, plus the 16-B over-reads of lds_swz
   __host__ __device__ static int stage_bytes(int w) {
     const int elems = VEC + SEG + w - 1 + E + 2 * VEC;
     const int bytes = elems * (int)sizeof(T);
     return (bytes + 1023) / 1024 * 1024;
   }
-  __host__ __device__ static int warp_bytes(int w, int ns) { return ns * stage_bytes(w) + 4 * AGG * (int)sizeof(T); }
+  __host__ __device__ static int warp_bytes(int w, int ns) { return ns * stage_bytes(w) + WarpAgg<T>::bytes(); }
   __host__ __device__ static size_t cta_bytes(int w, int ns) { return 1024 + (size_t)kStreamWarps * warp_bytes(w, ns); }
 };
 
@@ -125,7 +125,7 @@ struct StreamArgs {
   int64_t hld, chunk_ld, c, out_ld, streams;
   int64_t segs_per_row, nseg;
   int w, P;            // window; pad of the history rows
-  int qp, rp, V;       // gap geometry of block B = E*G (k1d_medium.cuh MedGeom)
+  WarpGeom g;          // gap geometry of block B = E*G (kwarp.cuh)
   int chunk_vec;       // chunk rows are 16-B aligned (else staged element-wise)
   int stage_bytes, warp_bytes;
   int nstages;         // staging ring per warp: 2..4 (nstages-1 segments in flight)
@@ -176,52 +176,35 @@ __device__ __forceinline__ void stream_stage(const StreamArgs &a, unsigned char 
   }
 }
 
-template <typename T, int G>
+template <typename T, int EE, int G>
 __global__ void __launch_bounds__(32 * kStreamWarps) k_stream_fused(StreamArgs a) {
-  using Geo = StreamGeo<T>;
+  using Geo = StreamGeo<T, EE>;
   constexpr int E = Geo::E;
   constexpr int SEG = Geo::SEG;
-  constexpr int B = E * G;
   constexpr int VEC = Geo::VEC;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *base = smem_align1024(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char *wb = base + warp * a.warp_bytes;
   auto stg = [&](int i) { return wb + i * a.stage_bytes; };
-  T *Gx = reinterpret_cast<T *>(wb + 2 * a.stage_bytes);
-  T *Gn = Gx + Geo::AGG;
-  T *Hx = Gn + Geo::AGG;
-  T *Hn = Hx + Geo::AGG;
+  const WarpAgg<T> agg(wb + a.nstages * a.stage_bytes);  // after the staging ring
   const int w = a.w, P = a.P;
-  const int gl = lane & (G - 1);
-  const int grp = lane / G;
-  const int glast = (lane & ~(G - 1)) + G - 1;
-  const int hstart = B - a.rp;
-  const int h_lane = hstart / E, h_off = hstart - (hstart / E) * E;
   const int64_t gw = blockIdx.x * (int64_t)kStreamWarps + warp, nw = (int64_t)gridDim.x * kStreamWarps;
 
   auto seg_pos = [&](int64_t sg, int64_t &row, int64_t &j0) {
-    row = sg / a.segs_per_row;
-    j0 = (sg - row * a.segs_per_row) * SEG;
+    if (a.segs_per_row == 1) {  // chunks of <= SEG samples: a segment is a stream
+      row = sg;
+      j0 = 0;
+    } else {  // nseg < 2^31 (checked by the launcher): 32-bit division
+      const uint32_t r = (uint32_t)sg / (uint32_t)a.segs_per_row;
+      row = r;
+      j0 = ((int64_t)sg - (int64_t)r * a.segs_per_row) * SEG;
+    }
   };
   auto seg_len = [&](int64_t j0) {  // staged elements of a segment
     const int64_t want = (int64_t)P + SEG + w - 1;
     const int64_t have = a.hld + a.c - j0;
     return (int)(want < have ? want : have);
-  };
-  auto h_part = [&](const T (&y)[E], T ax, T an, T bl, T &hx, T &hn) {
-    hx = hn = bl;
-    if (a.rp > 0) {
-      if (gl > h_lane) {
-        hx = Ord<T>::mx(hx, ax);
-        hn = Ord<T>::mn(hn, an);
-      } else if (gl == h_lane) {
-        T vx, vn;
-        suffix_from<T, E>(y, h_off, vx, vn);
-        hx = Ord<T>::mx(hx, vx);
-        hn = Ord<T>::mn(hn, vn);
-      }
-    }
   };
 
   const int ns = a.nstages;
@@ -234,8 +217,8 @@ __global__ void __launch_bounds__(32 * kStreamWarps) k_stream_fused(StreamArgs a
     }
     cp_async_commit();
   }
-  int it = 0, slot = 0;
-  for (int64_t sg = gw; sg < a.nseg; sg += nw, ++it) {
+  int slot = 0;
+  for (int64_t sg = gw; sg < a.nseg; sg += nw) {
     {  // keep ns-1 segments in flight
       const int64_t nx = sg + (ns - 1) * nw;
       if (nx < a.nseg) {
@@ -254,129 +237,22 @@ __global__ void __launch_bounds__(32 * kStreamWarps) k_stream_fused(StreamArgs a
     seg_pos(sg, row, j0);
     const int64_t left = a.c - j0;
     const int cnt = left < SEG ? (int)left : SEG;
-
-    // ---- far chunk: prefix (k1d_medium.cuh, same names)
-    T ux[E], un[E];
-    T cx, cn;
-    {
-      T y[E];
-      lds_swz<T, E>(X, P + lane * E + w - 1, y);
-      ux[0] = un[0] = y[0];
-#pragma unroll
-      for (int k = 1; k < E; ++k) {
-        ux[k] = Ord<T>::mx(ux[k - 1], y[k]);
-        un[k] = Ord<T>::mn(un[k - 1], y[k]);
-      }
-      T hx, hn;
-      h_part(y, ux[E - 1], un[E - 1], __shfl_sync(0xffffffffu, y[E - 1], glast), hx, hn);
-      grp_reduce<T, G>(hx, hn);
-      T ax = ux[E - 1], an = un[E - 1];
-      grp_scan_up<T, G>(ax, an, gl);
-      cx = shfl_up(ax, 1);
-      cn = shfl_up(an, 1);
-      if (gl == 0) {
-        cx = y[0];
-        cn = y[0];
-      }
-      if (gl == G - 1) {
-        Gx[a.V + grp] = ax;
-        Gn[a.V + grp] = an;
-        Hx[a.V + grp] = hx;
-        Hn[a.V + grp] = hn;
-      }
-    }
-    // ---- near chunk: suffix
-    {
-      T x[E];
-      lds_swz<T, E>(X, P + lane * E, x);
-      T sx = x[E - 1], sn = x[E - 1];
-      ux[E - 1] = Ord<T>::mx(ux[E - 1], sx);
-      un[E - 1] = Ord<T>::mn(un[E - 1], sn);
-#pragma unroll
-      for (int k = E - 2; k >= 0; --k) {
-        sx = Ord<T>::mx(sx, x[k]);
-        sn = Ord<T>::mn(sn, x[k]);
-        ux[k] = Ord<T>::mx(ux[k], sx);
-        un[k] = Ord<T>::mn(un[k], sn);
-      }
-      T bx = sx, bn = sn;
-      grp_scan_down<T, G>(bx, bn, gl);
-      T ex = shfl_down(bx, 1), en = shfl_down(bn, 1);
-      if (gl == G - 1) {
-        ex = x[E - 1];
-        en = x[E - 1];
-      }
-      cx = Ord<T>::mx(cx, ex);
-      cn = Ord<T>::mn(cn, en);
-    }
-    // ---- far blocks before the segment (always: segments carry nothing)
-    if (a.V > 0) {
-      const int nv = a.V * G;
-      for (int r0 = 0; r0 < nv; r0 += 32) {
-        const int vc = r0 + lane;
-        const int vcc = vc < nv ? vc : nv - 1;
-        const int gv = vcc / G;
-        T y[E];
-        lds_swz<T, E>(X, P + (gv - a.V) * B + w - 1 + gl * E, y);
-        T ax = y[0], an = y[0];
-#pragma unroll
-        for (int k = 1; k < E; ++k) {
-          ax = Ord<T>::mx(ax, y[k]);
-          an = Ord<T>::mn(an, y[k]);
-        }
-        T hx, hn;
-        h_part(y, ax, an, __shfl_sync(0xffffffffu, y[E - 1], glast), hx, hn);
-        grp_reduce<T, G>(ax, an);
-        grp_reduce<T, G>(hx, hn);
-        if (vc < nv && gl == 0) {
-          Gx[gv] = ax;
-          Gn[gv] = an;
-          Hx[gv] = hx;
-          Hn[gv] = hn;
-        }
-      }
-    }
-    __syncwarp();
-    // ---- gap + out
-    if (a.qp > 0 || a.rp > 0) {
-      const int b0 = a.V + grp - a.qp - 1;  // far block F_{g-q'-1}
-      T mx, mn;
-      if (a.rp > 0) {
-        mx = Hx[b0];
-        mn = Hn[b0];
+    T ox[E], on[E];
+    warp_window_med<T, E, G, false>(X, X, P, a.g, agg, lane, ox, on);
+    const int c0 = lane * E;
+    if (c0 < cnt) {
+      T *omx = a.out_max ? static_cast<T *>(a.out_max) + row * a.out_ld + j0 + c0 : nullptr;
+      T *omn = a.out_min ? static_cast<T *>(a.out_min) + row * a.out_ld + j0 + c0 : nullptr;
+      if (c0 + E <= cnt) {
+        if (omx) store_chunk<T, E>(omx, ox);
+        if (omn) store_chunk<T, E>(omn, on);
       } else {
-        mx = Gx[b0 + 1];
-        mn = Gn[b0 + 1];
-      }
-      for (int s = 1; s <= a.qp; ++s) {
-        mx = Ord<T>::mx(mx, Gx[b0 + s]);
-        mn = Ord<T>::mn(mn, Gn[b0 + s]);
-      }
-      cx = Ord<T>::mx(cx, mx);
-      cn = Ord<T>::mn(cn, mn);
-    }
-    {
-      T ox[E], on[E];
 #pragma unroll
-      for (int k = 0; k < E; ++k) {
-        ox[k] = Ord<T>::mx(ux[k], cx);
-        on[k] = Ord<T>::mn(un[k], cn);
-      }
-      const int c0 = lane * E;
-      if (c0 < cnt) {
-        T *omx = a.out_max ? static_cast<T *>(a.out_max) + row * a.out_ld + j0 + c0 : nullptr;
-        T *omn = a.out_min ? static_cast<T *>(a.out_min) + row * a.out_ld + j0 + c0 : nullptr;
-        if (c0 + E <= cnt) {
-          if (omx) store_chunk<T, E>(omx, ox);
-          if (omn) store_chunk<T, E>(omn, on);
-        } else {
-#pragma unroll
-          for (int k = 0; k < E; ++k)
-            if (c0 + k < cnt) {
-              if (omx) omx[k] = ox[k];
-              if (omn) omn[k] = on[k];
-            }
-        }
+        for (int k = 0; k < E; ++k)
+          if (c0 + k < cnt) {
+            if (omx) omx[k] = ox[k];
+            if (omn) omn[k] = on[k];
+          }
       }
     }
     // ---- the stream's last segment writes its new history: V'[c + t], t < hld
@@ -391,7 +267,7 @@ __global__ void __launch_bounds__(32 * kStreamWarps) k_stream_fused(StreamArgs a
         *reinterpret_cast<uint4 *>(ho + t) = u4;
       }
     }
-    __syncwarp();  // X is restaged by the next iteration; the aggregates too
+    __syncwarp();  // X is restaged by the next iteration
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
@@ -409,7 +285,7 @@ StreamLayout stream_layout(int64_t streams, int64_t w, int64_t max_chunk) {
   constexpr int VEC = 16 / (int)sizeof(T);
   auto up256 = [](size_t x) { return (x + 255) & ~size_t(255); };
   StreamLayout L;
-  L.fused = (w - 1 >= StreamGeo<T>::E && w - 1 <= kStreamHMax) ? 1 : 0;
+  L.fused = (w - 1 >= Chunk<T>::E && w - 1 <= kStreamHMax) ? 1 : 0;
   if (L.fused) {  // two history buffers (ping-pong), rows right-aligned
     L.ld = (w - 1 + VEC - 1) / VEC * VEC;
     L.hist_bytes = up256((size_t)streams * L.ld * sizeof(T));
@@ -424,15 +300,23 @@ StreamLayout stream_layout(int64_t streams, int64_t w, int64_t max_chunk) {
   return L;
 }
 
-template <typename T, int G>
+template <typename T, int E, int G>
 int launch_fused_g(StreamArgs a, cudaStream_t s) {
+  using Geo = StreamGeo<T, E>;
   // staging depth: the most segments in flight per SM (3 CTAs fit the registers)
+  // staging depth: the most segments in flight per SM (occupancy from registers and smem)
   int best = 2;
   {
     int64_t best_fly = -1;
     for (int ns = 2; ns <= 4; ++ns) {
-      const int64_t ctas = std::min<int64_t>(3, (int64_t)(220 * 1024) / (int64_t)StreamGeo<T>::cta_bytes(a.w, ns));
-      const int64_t fly = ctas * kStreamWarps * (ns - 1);
+      const size_t sm_bytes = Geo::cta_bytes(a.w, ns);
+      if (sm_bytes > 227 * 1024) continue;
+      cudaError_t e = cudaFuncSetAttribute(k_stream_fused<T, E, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes);
+      if (e != cudaSuccess) return note_cuda(e);
+      int per = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_stream_fused<T, E, G>, 32 * kStreamWarps, sm_bytes);
+      if (e != cudaSuccess) return note_cuda(e);
+      const int64_t fly = (int64_t)per * kStreamWarps * (ns - 1);
       if (fly > best_fly) {
         best_fly = fly;
         best = ns;
@@ -440,22 +324,26 @@ int launch_fused_g(StreamArgs a, cudaStream_t s) {
     }
   }
   a.nstages = best;
-  a.warp_bytes = StreamGeo<T>::warp_bytes(a.w, best);
-  const size_t smem = StreamGeo<T>::cta_bytes(a.w, best);
-  static int attr_set = 0;  // the largest dynamic smem size this instantiation was opened to
-  if ((int)smem > attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_stream_fused<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  a.stage_bytes = Geo::stage_bytes(a.w);
+  a.warp_bytes = Geo::warp_bytes(a.w, best);
+  a.segs_per_row = (a.c + Geo::SEG - 1) / Geo::SEG;
+  a.nseg = a.streams * a.segs_per_row;
+  if (a.nseg > 0x7fffffffLL) return kErrUnsupported;
+  a.g = make_warp_geom<E>(a.w, G);
+  if (a.g.V + 32 / G > WarpAgg<T>::AGG) return kErrUnsupported;
+  const size_t smem = Geo::cta_bytes(a.w, best);
+  {
+    cudaError_t e = cudaFuncSetAttribute(k_stream_fused<T, E, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return note_cuda(e);
-    attr_set = (int)smem;
   }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stream_fused<T, G>, 32 * kStreamWarps, smem);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stream_fused<T, E, G>, 32 * kStreamWarps, smem);
   if (e != cudaSuccess) return note_cuda(e);
   if (per_sm < 1) return kErrUnsupported;
   const int64_t want = (a.nseg + kStreamWarps - 1) / kStreamWarps;
   const int64_t cap = (int64_t)sm_count() * per_sm;
   const int grid = (int)(want < cap ? want : cap);
-  k_stream_fused<T, G><<<grid, 32 * kStreamWarps, smem, s>>>(a);
+  k_stream_fused<T, E, G><<<grid, 32 * kStreamWarps, smem, s>>>(a);
   return note_cuda(cudaGetLastError());
 }
 
@@ -466,7 +354,8 @@ int launch_stream_push(void *state, const StreamLayout &L, int64_t streams, int6
   constexpr int VEC = 16 / (int)sizeof(T);
   const int64_t h = w - 1;
   if (L.fused) {
-    using Geo = StreamGeo<T>;
+    constexpr int EB = Chunk<T>::E;                     // long chunks
+    constexpr int ES = EB / 2 >= VEC ? EB / 2 : EB;     // chunks of <= 32*ES samples: half the lanes' work
     char *base = static_cast<char *>(state);
     StreamArgs a;
     std::memset(&a, 0, sizeof(a));
@@ -480,27 +369,27 @@ int launch_stream_push(void *state, const StreamLayout &L, int64_t streams, int6
     a.c = c;
     a.out_ld = out_ld;
     a.streams = streams;
-    a.segs_per_row = (c + Geo::SEG - 1) / Geo::SEG;
-    a.nseg = streams * a.segs_per_row;
     a.w = (int)w;
     a.P = (int)(L.ld - h);
-    int G = 1;
-    while (G < 32 && Geo::E * G * 2 <= h) G *= 2;
-    const int B = Geo::E * G;
-    const int D = (int)h - B;
-    a.qp = D / B;
-    a.rp = D - a.qp * B;
-    a.V = a.qp + (a.rp > 0 ? 1 : 0);
-    if (a.V + 32 / G > Geo::AGG) return kErrUnsupported;
     a.chunk_vec = (reinterpret_cast<uintptr_t>(chunk) % 16 == 0 && (chunk_ld * (int64_t)sizeof(T)) % 16 == 0) ? 1 : 0;
-    a.stage_bytes = Geo::stage_bytes((int)w);
-    switch (G) {
-      case 1: return launch_fused_g<T, 1>(a, s);
-      case 2: return launch_fused_g<T, 2>(a, s);
-      case 4: return launch_fused_g<T, 4>(a, s);
-      case 8: return launch_fused_g<T, 8>(a, s);
-      case 16: return launch_fused_g<T, 16>(a, s);
-      default: return launch_fused_g<T, 32>(a, s);
+    const bool small_e = ES < EB && c <= 32 * ES && h >= ES;
+    if (small_e) {
+      switch (warp_group<ES>(w)) {
+        case 1: return launch_fused_g<T, ES, 1>(a, s);
+        case 2: return launch_fused_g<T, ES, 2>(a, s);
+        case 4: return launch_fused_g<T, ES, 4>(a, s);
+        case 8: return launch_fused_g<T, ES, 8>(a, s);
+        case 16: return launch_fused_g<T, ES, 16>(a, s);
+        default: return launch_fused_g<T, ES, 32>(a, s);
+      }
+    }
+    switch (warp_group<EB>(w)) {
+      case 1: return launch_fused_g<T, EB, 1>(a, s);
+      case 2: return launch_fused_g<T, EB, 2>(a, s);
+      case 4: return launch_fused_g<T, EB, 4>(a, s);
+      case 8: return launch_fused_g<T, EB, 8>(a, s);
+      case 16: return launch_fused_g<T, EB, 16>(a, s);
+      default: return launch_fused_g<T, EB, 32>(a, s);
     }
   }
   T *rows = static_cast<T *>(state);

@@ -468,6 +468,26 @@ def test_stream_odd_chunk_pitch(cuda_device):
     _stream_check(np.uint8, 64, 40, [256] * 3 + [13, 255], 256, seed=6, pitch=3)
 
 
+@pytest.mark.parametrize("w", [200, 600, 1025])
+def test_stream_many_segments_per_warp(cuda_device, w):
+    """Enough streams that every warp of the persistent grid runs many segments (its
+    staging ring and aggregate slots are reused) with a non-empty gap (w-1 not a block)."""
+    streams, c = 20000, 300
+    rows = synth.c3(rows=streams, length=4 * c)
+    st = mm.MaxMinStream(torch.float32, streams, w, c, device=dev())
+    x = torch.from_numpy(rows).to(dev())
+    exp = oracle.stream_pushes(rows[:64], w, [c] * 4)
+    k = np.random.default_rng(w).choice(streams, 64, replace=False)
+    expk = oracle.stream_pushes(rows[k], w, [c] * 4)
+    for p in range(4):
+        mx, mn, fv = st.push(x[:, p * c:(p + 1) * c].contiguous())
+        torch.cuda.synchronize()
+        assert_same(mx[:64, fv:], exp[p][0], f"max push {p}")
+        assert_same(mn[:64, fv:], exp[p][1], f"min push {p}")
+        assert_same(mx[k, fv:], expk[p][0], f"max push {p} sampled")
+        assert_same(mn[k, fv:], expk[p][1], f"min push {p} sampled")
+
+
 def test_stream_c3_full_size(cuda_device):
     """C3's 65 536 series as streams, 16 pushes of 256 samples, w=129 (the N2 bench
     workload): every window against the oracle's batch filter on the whole rows
@@ -489,3 +509,84 @@ def test_stream_c3_full_size(cuda_device):
     ex, en = oracle.batched(rows, w)
     assert_same(gx, ex, "C3 stream max")
     assert_same(gn, en, "C3 stream min")
+
+
+# ------------------------------------------------------------- N4: morphology
+MORPH_W = [1, 2, 3, 5, 8, 15, 16, 17, 18, 31, 33, 64, 129, 200, 513, 600, 1025]
+
+
+@pytest.mark.parametrize("w", MORPH_W)
+def test_morph_f32_windows(cuda_device, w):
+    n = 9_001  # several segments of 512 + a ragged tail
+    rows = np.stack([synth.c2(n, stream=s) for s in range(3)])
+    x = torch.from_numpy(rows).to(dev())
+    op, cl = mm.maxmin_morph_batched(x, w)
+    torch.cuda.synchronize()
+    for b in range(3):
+        eo, ec = oracle.morph(rows[b], w)
+        assert_same(op[b], eo, f"open row {b} w={w}")
+        assert_same(cl[b], ec, f"close row {b} w={w}")
+
+
+@pytest.mark.parametrize("dtype", DTYPES, ids=lambda d: np.dtype(d).name)
+def test_morph_every_dtype(cuda_device, dtype):
+    for w in (3, 8, 9, 16, 17, 100, 1000):
+        n = 5000
+        a = synth.random_values(np.dtype(dtype), 2 * n, seed=w)
+        rows = a.reshape(2, n)
+        x = torch.from_numpy(rows).to(dev())
+        op, cl = mm.maxmin_morph_batched(x, w)
+        torch.cuda.synchronize()
+        for b in range(2):
+            eo, ec = oracle.morph(rows[b], w)
+            assert_same(op[b], eo, f"open {np.dtype(dtype).name} w={w}")
+            assert_same(cl[b], ec, f"close {np.dtype(dtype).name} w={w}")
+
+
+@pytest.mark.parametrize("n_minus_w", [0, 1, 2, 100])
+@pytest.mark.parametrize("w", [1, 4, 17, 300])
+def test_morph_short_rows_and_brute(cuda_device, w, n_minus_w):
+    n = w + n_minus_w
+    a = synth.random_values(np.float32, n, seed=n)
+    x = torch.from_numpy(a).to(dev())
+    op, cl = mm.maxmin_morph_1d(x, w)
+    torch.cuda.synchronize()
+    eo, ec = oracle.morph(a, w, brute=n * w * w < 3e7)
+    assert_same(op, eo, "open")
+    assert_same(cl, ec, "close")
+
+
+def test_morph_strided_rows_and_one_output(cuda_device):
+    rows = synth.c3(rows=50, length=1000, ld=1003)  # odd input pitch: element-wise staging
+    x = torch.from_numpy(rows).to(dev())
+    op, _ = mm.maxmin_morph_batched(x, 129, n=1000, want_close=False)
+    _, cl = mm.maxmin_morph_batched(x, 129, n=1000, want_open=False)
+    torch.cuda.synchronize()
+    for b in (0, 17, 49):
+        eo, ec = oracle.morph(rows[b, :1000], 129)
+        assert_same(op[b], eo, "open")
+        assert_same(cl[b], ec, "close")
+
+
+def test_morph_c3_full_size_sampled(cuda_device):
+    """C3's 65 536 x 4096 series, w=129 (the N4 bench workload): 300 sampled rows."""
+    rows = synth.c3()
+    x = torch.from_numpy(rows).to(dev())
+    op, cl = mm.maxmin_morph_batched(x, 129)
+    torch.cuda.synchronize()
+    for b in np.random.default_rng(2).choice(rows.shape[0], 300, replace=False):
+        eo, ec = oracle.morph(rows[b], 129)
+        assert_same(op[b], eo, f"open row {b}")
+        assert_same(cl[b], ec, f"close row {b}")
+
+
+@pytest.mark.parametrize("wr,wc", [(1, 1), (3, 3), (5, 2), (1, 7), (15, 15), (16, 16), (4, 9)])
+@pytest.mark.parametrize("dtype", [np.uint8, np.float32, np.int64], ids=lambda d: np.dtype(d).name)
+def test_morph_2d(cuda_device, wr, wc, dtype):
+    a = synth.random_values(np.dtype(dtype), 2 * 70 * 90, seed=wr * 31 + wc).reshape(2, 70, 90)
+    x = torch.from_numpy(a).to(dev())
+    op, cl = mm.maxmin_morph_2d(x, wr, wc)
+    torch.cuda.synchronize()
+    eo, ec = oracle.morph_2d(a, wr, wc)
+    assert_same(op, eo, "open 2d")
+    assert_same(cl, ec, "close 2d")
