@@ -269,8 +269,9 @@ int launch_morph_g(MorphArgs a, cudaStream_t s) {
       int per = 0;
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_morph_fused<T, G>, 32 * nwb, bytes);
       if (e != cudaSuccess) return note_cuda(e);
-      const int64_t fly = (int64_t)per * nwb * (ns - 1);
-      if (fly > best_fly) {
+      // instruction-latency bound: resident warps first, then segments in flight
+      const int64_t fly = ((int64_t)per * nwb) * 8 + (ns - 1);
+      if (per > 0 && fly > best_fly) {
         best_fly = fly;
         best_ns = ns;
         best_nw = nwb;
