@@ -156,7 +156,8 @@ def maxmin_argfilter_batched(x: torch.Tensor, w: int, n: int | None = None, *, w
     batch, ncols = x.shape
     n = ncols if n is None else n
     m = max(n - w + 1, 0)
-    mk = lambda dt: torch.empty(batch, max(m, 1), dtype=dt, device=x.device)[:, :m]  # noqa: E731
+    out_ld = max((m + 15) // 16 * 16, 16)  # 16-B rows for every output dtype: vector stores
+    mk = lambda dt: torch.empty(batch, out_ld, dtype=dt, device=x.device)[:, :m]  # noqa: E731
     out_max = mk(x.dtype) if want_max and values else None
     out_min = mk(x.dtype) if want_min and values else None
     arg_max = mk(torch.int64) if want_max else None
@@ -164,7 +165,6 @@ def maxmin_argfilter_batched(x: torch.Tensor, w: int, n: int | None = None, *, w
     need = maxmin_argfilter_workspace_bytes(x.dtype, batch, n, w)
     if workspace is None:
         workspace = torch.empty(max(need, 16), dtype=torch.uint8, device=x.device)
-    out_ld = max(m, 1)
     _lib.check(_lib.lib().maxmin_argfilter_batched(
         dtype_code(x.dtype), _ptr(x), batch, n, x.stride(0), w, _ptr(out_max), _ptr(out_min),
         _ptr(arg_max), _ptr(arg_min), out_ld, _ptr(workspace), workspace.numel() * workspace.element_size(),

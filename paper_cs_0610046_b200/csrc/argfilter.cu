@@ -14,9 +14,16 @@
 // (floats: the sign-magnitude flip; +-0 both map to +0's code, reading R8).
 // Three steps, all on the GPU: keys (elementwise), the max filter on kx and
 // the min filter on kn (k1d_small/medium/large<uint64_t>), decode
-// (elementwise).  The keys and the key outputs live in the workspace.  This is
-// a composition, not a fused pass: ~92 B of HBM traffic per element against
-// ~28 B for a fused kernel (N1).
+// (elementwise).  The keys and the key outputs live in the workspace: ~92 B of
+// HBM traffic per element.
+//
+// Fused path (w-1 <= kArgHMax, aligned outputs; k_arg_fused): the keys never
+// reach memory.  Warp-autonomous like the stream and morphology kernels
+// (kwarp.cuh): a warp stages the raw values of its 256 windows plus the w-1
+// halo with cp.async and builds both keys on the fly inside the loads
+// (ArgLoader), so the traffic is the contract's: the input once, the values
+// and the int64 positions out once (4n + 24m bytes for f32).
+#include "kwarp.cuh"
 #include "launch.cuh"
 
 namespace mm {
@@ -114,7 +121,16 @@ int grid_for(int64_t items) {
 }
 }  // namespace
 
-size_t argfilter_workspace(int64_t batch, int64_t n, int64_t w) { return arg_layout(batch, n, w).total; }
+constexpr int kArgFusedHMax = 1024;  // = kArgHMax below: the fused path needs no workspace
+size_t argfilter_workspace(int64_t batch, int64_t n, int64_t w) {
+  const int64_t m = n - w + 1;
+  if (w - 1 <= kArgFusedHMax && batch * ((m + 255) / 256) <= 0x7fffffffLL) return 0;
+  return arg_layout(batch, n, w).total;
+}
+
+template <typename S>
+int launch_arg_fused(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w, void *out_max, void *out_min,
+                     int64_t *arg_max, int64_t *arg_min, int64_t out_ld, cudaStream_t s);
 
 template <typename T>
 int launch_argfilter(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w, void *out_max,
@@ -122,6 +138,10 @@ int launch_argfilter(const void *in, int64_t batch, int64_t n, int64_t in_ld, in
                      size_t ws_bytes, cudaStream_t s) {
   static_assert(sizeof(T) <= 4, "keys hold a 32-bit order code and a 32-bit position");
   if (batch == 0) return kOK;
+  {
+    const int rc = launch_arg_fused<T>(in, batch, n, in_ld, w, out_max, out_min, arg_max, arg_min, out_ld, s);
+    if (rc != kErrUnsupported) return rc;
+  }
   const ArgLayout L = arg_layout(batch, n, w);
   if (!ws || ws_bytes < L.total) return kErrWorkspace;
   char *p = static_cast<char *>(ws);
@@ -149,6 +169,266 @@ int launch_argfilter(const void *in, int64_t batch, int64_t n, int64_t in_ld, in
                                                     batch, m, L.mld, static_cast<T *>(out_max),
                                                     static_cast<T *>(out_min), arg_max, arg_min, out_ld);
   return note_cuda(cudaGetLastError());
+}
+
+// ============================================================ fused path
+constexpr int kArgHMax = kArgFusedHMax;  // largest w-1 of k_arg_fused
+constexpr int kArgWarps = 4;
+
+// the two keys of the staged values at logical positions pos.. (absolute base+pos..)
+template <typename S>
+struct ArgLoader {
+  const unsigned char *X;
+  uint32_t base;
+  static constexpr bool TWO = true;
+  template <int N>
+  __device__ __forceinline__ void load(int pos, uint64_t (&ya)[N], uint64_t (&yb)[N]) const {
+    S v[N];
+    lds_swz<S, N>(X, pos, v);
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const uint64_t o = (uint64_t)ord32<S>(v[k]) << 32;
+      const uint32_t i = base + (uint32_t)(pos + k);
+      ya[k] = o | (0xffffffffu - i);
+      yb[k] = o | i;
+    }
+  }
+};
+
+template <typename S>
+struct ArgGeo {
+  static constexpr int E = 8;  // 8-byte keys
+  static constexpr int SEG = 32 * E;
+  static constexpr int VEC = 16 / (int)sizeof(S);
+  __host__ __device__ static int stage_bytes(int w) {
+    return ((SEG + w - 1 + 2 * E + 2 * VEC + 16) * (int)sizeof(S) + 127) / 128 * 128;
+  }
+  __host__ __device__ static int warp_bytes(int w, int ns) { return ns * stage_bytes(w) + WarpAgg<uint64_t>::bytes(); }
+  __host__ __device__ static size_t cta_bytes(int w, int ns, int nw) { return 1024 + (size_t)nw * warp_bytes(w, ns); }
+};
+
+struct ArgArgs {
+  const void *in;
+  void *out_max, *out_min;
+  int64_t *arg_max, *arg_min;
+  int64_t n, m, in_ld, out_ld, batch, segs_per_row, nseg;
+  WarpGeom g;
+  int w, in_vec, out_vec, stage_bytes, warp_bytes, nstages;
+};
+
+__device__ __forceinline__ void acp_async16(void *smem, const void *g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void acp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void acp_async_wait_ring(int n) {
+  if (n >= 4)
+    asm volatile("cp.async.wait_group 3;" ::: "memory");
+  else if (n == 3)
+    asm volatile("cp.async.wait_group 2;" ::: "memory");
+  else
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+}
+
+template <typename S>
+__device__ __forceinline__ void arg_stage(const ArgArgs &a, unsigned char *X, int64_t row, int64_t j0, int lane) {
+  constexpr int VEC = 16 / (int)sizeof(S);
+  const int64_t want = j0 + ArgGeo<S>::SEG + a.w - 1;
+  const int64_t end = want < a.n ? want : a.n;
+  const int nq = (int)((end - j0 + VEC - 1) / VEC);
+  const S *src = static_cast<const S *>(a.in) + row * a.in_ld;
+  for (int q = lane; q < nq; q += 32) {
+    const int64_t v = j0 + (int64_t)q * VEC;
+    unsigned char *dst = X + swz(q);
+    if (a.in_vec && v + VEC <= a.n) {
+      acp_async16(dst, src + v);
+    } else {
+      S t[VEC];
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) t[k] = v + k < a.n ? src[v + k] : S(0);
+      uint4 u4;
+      memcpy(&u4, t, 16);
+      *reinterpret_cast<uint4 *>(dst) = u4;
+    }
+  }
+}
+
+template <typename S, int G>
+__global__ void __launch_bounds__(32 * kArgWarps) k_arg_fused(ArgArgs a) {
+  using Geo = ArgGeo<S>;
+  constexpr int E = Geo::E;
+  constexpr int SEG = Geo::SEG;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *base = smem_align1024(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char *wb = base + warp * a.warp_bytes;
+  auto stg = [&](int i) { return wb + i * a.stage_bytes; };
+  const WarpAgg<uint64_t> agg(wb + a.nstages * a.stage_bytes);
+  const int nwb = blockDim.x >> 5;
+  const int64_t gw = blockIdx.x * (int64_t)nwb + warp, nw = (int64_t)gridDim.x * nwb;
+  auto seg_pos = [&](int64_t sg, int64_t &row, int64_t &j0) {  // nseg < 2^31 (launcher)
+    const uint32_t r = (uint32_t)sg / (uint32_t)a.segs_per_row;
+    row = r;
+    j0 = ((int64_t)sg - (int64_t)r * a.segs_per_row) * SEG;
+  };
+  const int ns = a.nstages;
+  for (int k = 0; k + 1 < ns; ++k) {
+    const int64_t sg = gw + k * nw;
+    if (sg < a.nseg) {
+      int64_t row, j0;
+      seg_pos(sg, row, j0);
+      arg_stage<S>(a, stg(k), row, j0, lane);
+    }
+    acp_async_commit();
+  }
+  int slot = 0;
+  for (int64_t sg = gw; sg < a.nseg; sg += nw) {
+    {
+      const int64_t nx = sg + (ns - 1) * nw;
+      if (nx < a.nseg) {
+        int64_t row, j0;
+        seg_pos(nx, row, j0);
+        arg_stage<S>(a, stg(slot + ns - 1 < ns ? slot + ns - 1 : slot - 1), row, j0, lane);
+      }
+    }
+    acp_async_commit();
+    acp_async_wait_ring(ns);
+    __syncwarp();
+    const unsigned char *X = stg(slot);
+    slot = slot + 1 < ns ? slot + 1 : 0;
+    int64_t row, j0;
+    seg_pos(sg, row, j0);
+    uint64_t kx[E], kn[E];
+    const ArgLoader<S> ld{X, (uint32_t)j0};
+    if constexpr (G == 0)
+      warp_window_small<uint64_t, E>(ld, 0, a.w, lane, kx, kn);
+    else
+      warp_window_med<uint64_t, E, G>(ld, 0, a.g, agg, lane, kx, kn);
+    const int64_t j = j0 + lane * E;
+    const int64_t left = a.m - j;
+    if (left > 0) {
+      const int64_t o = row * a.out_ld + j;
+      S vx[E], vn[E];
+      int64_t ix[E], in_[E];
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        vx[k] = unord32<S>((uint32_t)(kx[k] >> 32));
+        ix[k] = (int64_t)(0xffffffffu - (uint32_t)kx[k]);
+        vn[k] = unord32<S>((uint32_t)(kn[k] >> 32));
+        in_[k] = (int64_t)(uint32_t)kn[k];
+      }
+      S *omx = a.out_max ? static_cast<S *>(a.out_max) + o : nullptr;
+      S *omn = a.out_min ? static_cast<S *>(a.out_min) + o : nullptr;
+      int64_t *oax = a.arg_max ? a.arg_max + o : nullptr;
+      int64_t *oan = a.arg_min ? a.arg_min + o : nullptr;
+      if (left >= E && a.out_vec) {
+        if constexpr ((E * sizeof(S)) % 16 == 0) {
+          if (omx) store_chunk<S, E>(omx, vx);
+          if (omn) store_chunk<S, E>(omn, vn);
+        } else {
+#pragma unroll
+          for (int k = 0; k < E; ++k) {
+            if (omx) omx[k] = vx[k];
+            if (omn) omn[k] = vn[k];
+          }
+        }
+        if (oax) store_chunk<int64_t, E>(oax, ix);
+        if (oan) store_chunk<int64_t, E>(oan, in_);
+      } else {
+#pragma unroll
+        for (int k = 0; k < E; ++k)
+          if (k < left) {
+            if (omx) omx[k] = vx[k];
+            if (omn) omn[k] = vn[k];
+            if (oax) oax[k] = ix[k];
+            if (oan) oan[k] = in_[k];
+          }
+      }
+    }
+    __syncwarp();
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+template <typename S, int G>
+int launch_arg_g(ArgArgs a, cudaStream_t s) {
+  using Geo = ArgGeo<S>;
+  int best_ns = 0, best_nw = 0;
+  int64_t best = -1;
+  for (int nwb = kArgWarps; nwb >= 1; nwb /= 2) {
+    for (int ns = 2; ns <= 4; ++ns) {
+      const size_t bytes = Geo::cta_bytes(a.w, ns, nwb);
+      if (bytes > 227 * 1024) continue;
+      cudaError_t e = cudaFuncSetAttribute(k_arg_fused<S, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      if (e != cudaSuccess) return note_cuda(e);
+      int per = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_arg_fused<S, G>, 32 * nwb, bytes);
+      if (e != cudaSuccess) return note_cuda(e);
+      const int64_t score = ((int64_t)per * nwb) * 8 + (ns - 1);  // resident warps first
+      if (per > 0 && score > best) {
+        best = score;
+        best_ns = ns;
+        best_nw = nwb;
+      }
+    }
+  }
+  if (best < 0) return kErrUnsupported;
+  a.nstages = best_ns;
+  a.stage_bytes = Geo::stage_bytes(a.w);
+  a.warp_bytes = Geo::warp_bytes(a.w, best_ns);
+  const size_t smem = Geo::cta_bytes(a.w, best_ns, best_nw);
+  cudaError_t e = cudaFuncSetAttribute(k_arg_fused<S, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return note_cuda(e);
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_arg_fused<S, G>, 32 * best_nw, smem);
+  if (e != cudaSuccess) return note_cuda(e);
+  const int64_t want = (a.nseg + best_nw - 1) / best_nw;
+  const int64_t cap = (int64_t)sm_count() * per_sm;
+  k_arg_fused<S, G><<<(int)(want < cap ? want : cap), 32 * best_nw, smem, s>>>(a);
+  return note_cuda(cudaGetLastError());
+}
+
+// kErrUnsupported when the fused path does not apply (the caller composes)
+template <typename S>
+int launch_arg_fused(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w, void *out_max, void *out_min,
+                     int64_t *arg_max, int64_t *arg_min, int64_t out_ld, cudaStream_t s) {
+  using Geo = ArgGeo<S>;
+  constexpr int E = Geo::E;
+  if (w - 1 > kArgHMax) return kErrUnsupported;
+  ArgArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.in = in;
+  a.out_max = out_max;
+  a.out_min = out_min;
+  a.arg_max = arg_max;
+  a.arg_min = arg_min;
+  a.n = n;
+  a.m = n - w + 1;
+  a.in_ld = in_ld;
+  a.out_ld = out_ld;
+  a.batch = batch;
+  a.segs_per_row = (a.m + Geo::SEG - 1) / Geo::SEG;
+  a.nseg = batch * a.segs_per_row;
+  if (a.nseg > 0x7fffffffLL) return kErrUnsupported;
+  a.w = (int)w;
+  a.in_vec = (reinterpret_cast<uintptr_t>(in) % 16 == 0 && (in_ld * (int64_t)sizeof(S)) % 16 == 0) ? 1 : 0;
+  auto al = [](const void *p) { return p == nullptr || reinterpret_cast<uintptr_t>(p) % 16 == 0; };
+  a.out_vec = (al(out_max) && al(out_min) && al(arg_max) && al(arg_min) && (out_ld * 8) % 16 == 0 &&
+               (out_ld * (int64_t)sizeof(S)) % 16 == 0) ? 1 : 0;
+  if (w - 1 < E) {
+    a.g.w = (int)w;
+    return launch_arg_g<S, 0>(a, s);
+  }
+  const int G = warp_group<E>(w);
+  a.g = make_warp_geom<E>((int)w, G);
+  if (a.g.V + 32 / G > WarpAgg<uint64_t>::AGG) return kErrUnsupported;
+  switch (G) {
+    case 1: return launch_arg_g<S, 1>(a, s);
+    case 2: return launch_arg_g<S, 2>(a, s);
+    case 4: return launch_arg_g<S, 4>(a, s);
+    case 8: return launch_arg_g<S, 8>(a, s);
+    case 16: return launch_arg_g<S, 16>(a, s);
+    default: return launch_arg_g<S, 32>(a, s);
+  }
 }
 
 #define MM_ARG_INST(T)                                                                           \

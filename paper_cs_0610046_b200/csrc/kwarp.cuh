@@ -5,9 +5,10 @@
 //
 // For lane l and k < E the warp computes the 32E consecutive windows starting
 // at logical positions p = pos0 + l*E + k:
-//     ox[k] = max XA[p .. p+w)        on[k] = min XB[p .. p+w)
-// (XA == XB for a max-min filter; the morphology's second pass takes the max
-// over the erosion buffer and the min over the dilation buffer).
+//     ox[k] = max A[p .. p+w)        on[k] = min B[p .. p+w)
+// where a loader supplies A and B (the same staged buffer for the max-min
+// filter; the arg filter's (value, position) keys, built on the fly from the
+// staged values, for N1).  warp_window_med1 / warp_window_small1: one chain.
 //
 //   warp_window_med<G>: E <= w-1.  The near/far decomposition of k1d_medium
 //     (k1d_medium.cuh, same names): block B = E*G <= w-1, out = max(S, gap, P)
@@ -67,10 +68,24 @@ struct WarpAgg {
   static constexpr int bytes() { return 4 * AGG * (int)sizeof(T); }
 };
 
-template <typename T, int E, int G, bool TWO>
-__device__ __forceinline__ void warp_window_med(const unsigned char *XA, const unsigned char *XB, int pos0,
-                                                const WarpGeom &g, const WarpAgg<T> &agg, int lane, T (&ox)[E],
-                                                T (&on)[E]) {
+// Loaders: ld.load<N>(pos, ya, yb) fills the N values of the max chain (ya) and
+// of the min chain (yb) at logical positions pos .. pos+N-1.
+template <typename T>
+struct PairLoader {  // the max-min filter: both chains read the same staged buffer
+  const unsigned char *X;
+  static constexpr bool TWO = false;
+  template <int N>
+  __device__ __forceinline__ void load(int pos, T (&ya)[N], T (&yb)[N]) const {
+    lds_swz<T, N>(X, pos, ya);
+#pragma unroll
+    for (int k = 0; k < N; ++k) yb[k] = ya[k];
+  }
+};
+
+template <typename T, int E, int G, class Ld>
+__device__ __forceinline__ void warp_window_med(const Ld &ld, int pos0, const WarpGeom &g, const WarpAgg<T> &agg,
+                                                int lane, T (&ox)[E], T (&on)[E]) {
+  constexpr bool TWO = Ld::TWO;
   constexpr int B = E * G;
   const int w = g.w;
   const int gl = lane & (G - 1);
@@ -96,13 +111,7 @@ __device__ __forceinline__ void warp_window_med(const unsigned char *XA, const u
   T cx, cn;
   {  // ---- far chunk: prefix
     T ya[E], yb[E];
-    lds_swz<T, E>(XA, pos0 + lane * E + w - 1, ya);
-    if (TWO) {
-      lds_swz<T, E>(XB, pos0 + lane * E + w - 1, yb);
-    } else {
-#pragma unroll
-      for (int k = 0; k < E; ++k) yb[k] = ya[k];
-    }
+    ld.template load<E>(pos0 + lane * E + w - 1, ya, yb);
     ux[0] = ya[0];
     un[0] = yb[0];
 #pragma unroll
@@ -132,13 +141,7 @@ __device__ __forceinline__ void warp_window_med(const unsigned char *XA, const u
   }
   {  // ---- near chunk: suffix
     T xa[E], xb[E];
-    lds_swz<T, E>(XA, pos0 + lane * E, xa);
-    if (TWO) {
-      lds_swz<T, E>(XB, pos0 + lane * E, xb);
-    } else {
-#pragma unroll
-      for (int k = 0; k < E; ++k) xb[k] = xa[k];
-    }
+    ld.template load<E>(pos0 + lane * E, xa, xb);
     T sx = xa[E - 1], sn = xb[E - 1];
     ux[E - 1] = Ord<T>::mx(ux[E - 1], sx);
     un[E - 1] = Ord<T>::mn(un[E - 1], sn);
@@ -167,13 +170,7 @@ __device__ __forceinline__ void warp_window_med(const unsigned char *XA, const u
       const int gv = vcc / G;
       const int pos = pos0 + (gv - g.V) * B + w - 1 + gl * E;
       T ya[E], yb[E];
-      lds_swz<T, E>(XA, pos, ya);
-      if (TWO) {
-        lds_swz<T, E>(XB, pos, yb);
-      } else {
-#pragma unroll
-        for (int k = 0; k < E; ++k) yb[k] = ya[k];
-      }
+      ld.template load<E>(pos, ya, yb);
       T ax = ya[0], an = yb[0];
 #pragma unroll
       for (int k = 1; k < E; ++k) {
@@ -268,18 +265,11 @@ __device__ __forceinline__ void small_k(const T (&va)[2 * E], const T (&vb)[2 * 
   }
 }
 
-template <typename T, int E, bool TWO>
-__device__ __forceinline__ void warp_window_small(const unsigned char *XA, const unsigned char *XB, int pos0, int w,
-                                                  int lane, T (&ox)[E], T (&on)[E]) {
+template <typename T, int E, class Ld>
+__device__ __forceinline__ void warp_window_small(const Ld &ld, int pos0, int w, int lane, T (&ox)[E], T (&on)[E]) {
   static_assert(E <= 16, "span levels up to 2^4");
   T va[2 * E], vb[2 * E];
-  lds_swz<T, 2 * E>(XA, pos0 + lane * E, va);
-  if (TWO) {
-    lds_swz<T, 2 * E>(XB, pos0 + lane * E, vb);
-  } else {
-#pragma unroll
-    for (int p = 0; p < 2 * E; ++p) vb[p] = va[p];
-  }
+  ld.template load<2 * E>(pos0 + lane * E, va, vb);
   const int K = 31 - __clz(w);  // 2^K <= w < 2^(K+1), w <= E
   const int d = w - (1 << K);
   switch (K) {  // warp-uniform

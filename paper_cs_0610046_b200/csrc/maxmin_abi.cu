@@ -325,22 +325,23 @@ int maxmin_argfilter_batched(int dt, const void *in, int64_t batch, int64_t n, i
   auto el = [](const void *q, uintptr_t a) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) % a) == 0; };
   if (!el(in, sz) || !el(out_max, sz) || !el(out_min, sz) || !el(arg_max, 8) || !el(arg_min, 8))
     return MAXMIN_ERR_ALIGNMENT;
-  if (!workspace || workspace_bytes < need || !aligned16(workspace)) return MAXMIN_ERR_WORKSPACE;
+  if (need > 0 && (!workspace || workspace_bytes < need || !aligned16(workspace))) return MAXMIN_ERR_WORKSPACE;
   if (batch == 0) return MAXMIN_OK;
+  if (need == 0) workspace = nullptr;  // the fused path: nothing to check or touch
   const void *outs[4] = {out_max, out_min, arg_max, arg_min};
   const size_t obytes[4] = {ob, ob, ab, ab};
   for (int i = 0; i < 4; ++i) {
     if (!outs[i]) continue;
-    if (overlap(in, ib, outs[i], obytes[i]) || overlap(workspace, need, outs[i], obytes[i]))
+    if (overlap(in, ib, outs[i], obytes[i]) || (workspace && overlap(workspace, need, outs[i], obytes[i])))
       return MAXMIN_ERR_ALIAS;
     for (int k = i + 1; k < 4; ++k)
       if (outs[k] && overlap(outs[i], obytes[i], outs[k], obytes[k])) return MAXMIN_ERR_ALIAS;
   }
-  if (overlap(workspace, need, in, ib)) return MAXMIN_ERR_ALIAS;
+  if (workspace && overlap(workspace, need, in, ib)) return MAXMIN_ERR_ALIAS;
   if ((rc = ensure_device(in)) != MAXMIN_OK) return rc;
   for (int i = 0; i < 4; ++i)
     if (outs[i] && (rc = ensure_device(outs[i])) != MAXMIN_OK) return rc;
-  if ((rc = ensure_device(workspace)) != MAXMIN_OK) return rc;
+  if (workspace && (rc = ensure_device(workspace)) != MAXMIN_OK) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   switch (dt) {
     case MAXMIN_U8: return mm::launch_argfilter<uint8_t>(in, batch, n, in_ld, w, out_max, out_min, arg_max, arg_min, out_ld, workspace, workspace_bytes, s);

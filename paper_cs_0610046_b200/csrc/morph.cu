@@ -46,17 +46,22 @@ __device__ __forceinline__ T highest_value() {
   else return std::numeric_limits<T>::max();
 }
 
+#ifndef MM_MORPH_E
+#define MM_MORPH_E 16
+#endif
 template <typename T>
 struct MorphGeo {
-  // 8 elements per lane (16 for bytes: one 16-B unit): ~100 registers, more warps in flight
-  static constexpr int E = sizeof(T) == 1 ? 16 : 8;
+  // elements per lane (<= Chunk<T>::E; at least one 16-B unit)
+  static constexpr int E = (MM_MORPH_E < Chunk<T>::E ? (MM_MORPH_E * (int)sizeof(T) >= 16 ? MM_MORPH_E : 16 / (int)sizeof(T))
+                                                     : Chunk<T>::E);
   static constexpr int VEC = 16 / (int)sizeof(T);
   static constexpr int SEG = 32 * E;
-  __host__ __device__ static int round1k(int bytes) { return (bytes + 127) / 128 * 128; }  // 128-B rows
-  // staged input: P1 + (rounds of pass 1) + w - 1 + over-reads
-  __host__ __device__ static int stage_bytes(int w) { return round1k((3 * VEC + 2 * SEG + 2 * w + 2 * E) * (int)sizeof(T)); }
-  // e / d buffers: rounds of pass 1 (<= 2*SEG + w) + pass-2 over-reads
-  __host__ __device__ static int ebuf_bytes(int w) { return round1k((2 * SEG + w + 2 * E + 2 * VEC) * (int)sizeof(T)); }
+  __host__ __device__ static int round128(int bytes) { return (bytes + 127) / 128 * 128; }
+  // offset of position j0 in the erosion / dilation buffers (the w-1 carried before it)
+  __host__ __device__ static int off(int w) { return (w - 1 + VEC - 1) / VEC * VEC; }
+  // staged input f[j0, j0 + SEG + w - 1) + over-reads
+  __host__ __device__ static int stage_bytes(int w) { return round128((SEG + w + E + 2 * VEC) * (int)sizeof(T)); }
+  __host__ __device__ static int ebuf_bytes(int w) { return round128((off(w) + SEG + E + 2 * VEC) * (int)sizeof(T)); }
   __host__ __device__ static int warp_bytes(int w, int ns) {
     return ns * stage_bytes(w) + 2 * ebuf_bytes(w) + WarpAgg<T>::bytes();
   }
@@ -90,37 +95,24 @@ __device__ __forceinline__ void mcp_async_wait_ring(int n) {
     asm volatile("cp.async.wait_group 1;" ::: "memory");
 }
 
-// first staged position of segment j0 (16-B aligned, may be negative) and the
-// offset P1 of a[j0-(w-1)] in the staged buffer
-__device__ __forceinline__ void morph_base(int64_t j0, int w, int vec, int64_t &a0, int &p1) {
-  const int64_t s = j0 - (w - 1);
-  p1 = (int)(((s % vec) + vec) % vec);
-  a0 = s - p1;
-}
-
+// stage f[j0, j0 + SEG + w - 1) of `row` (j0 is a multiple of SEG: 16-B aligned)
 template <typename T>
 __device__ __forceinline__ void morph_stage(const MorphArgs &a, unsigned char *X, int64_t row, int64_t j0, int lane) {
   constexpr int VEC = 16 / (int)sizeof(T);
   constexpr int SEG = MorphGeo<T>::SEG;
-  int64_t a0;
-  int p1;
-  morph_base(j0, a.w, VEC, a0, p1);
-  const int64_t want_end = j0 + SEG + a.w - 1;  // exclusive
+  const int64_t want_end = j0 + SEG + a.w - 1;
   const int64_t end = want_end < a.n ? want_end : a.n;
-  const int nq = (int)((end - a0 + VEC - 1) / VEC);
+  const int nq = (int)((end - j0 + VEC - 1) / VEC);
   const T *src = static_cast<const T *>(a.in) + row * a.in_ld;
   for (int q = lane; q < nq; q += 32) {
-    const int64_t v = a0 + (int64_t)q * VEC;
+    const int64_t v = j0 + (int64_t)q * VEC;
     unsigned char *dst = X + swz(q);
-    if (a.in_vec && v >= 0 && v + VEC <= a.n) {
+    if (a.in_vec && v + VEC <= a.n) {
       mcp_async16(dst, src + v);
     } else {
       T t[VEC];
 #pragma unroll
-      for (int k = 0; k < VEC; ++k) {
-        const int64_t u = v + k;
-        t[k] = (u >= 0 && u < a.n) ? src[u] : T(0);
-      }
+      for (int k = 0; k < VEC; ++k) t[k] = v + k < a.n ? src[v + k] : T(0);
       uint4 u4;
       memcpy(&u4, t, 16);
       *reinterpret_cast<uint4 *>(dst) = u4;
@@ -141,14 +133,13 @@ __device__ __forceinline__ void sts_swz_chunk(unsigned char *buf, int pos, const
   }
 }
 
-template <typename T, int E, int G, bool TWO>
-__device__ __forceinline__ void morph_window(const unsigned char *XA, const unsigned char *XB, int pos0,
-                                             const WarpGeom &g, const WarpAgg<T> &agg, int lane, T (&ox)[E],
-                                             T (&on)[E]) {
+template <typename T, int E, int G>
+__device__ __forceinline__ void morph_window(const unsigned char *X, int pos0, const WarpGeom &g,
+                                             const WarpAgg<T> &agg, int lane, T (&ox)[E], T (&on)[E]) {
   if constexpr (G == 0)
-    warp_window_small<T, E, TWO>(XA, XB, pos0, g.w, lane, ox, on);
+    warp_window_small<T, E>(PairLoader<T>{X}, pos0, g.w, lane, ox, on);
   else
-    warp_window_med<T, E, G, TWO>(XA, XB, pos0, g, agg, lane, ox, on);
+    warp_window_med<T, E, G>(PairLoader<T>{X}, pos0, g, agg, lane, ox, on);
 }
 
 template <typename T, int G>
@@ -156,29 +147,38 @@ __global__ void __launch_bounds__(32 * kMorphWarps) k_morph_fused(MorphArgs a) {
   using Geo = MorphGeo<T>;
   constexpr int E = Geo::E;
   constexpr int SEG = Geo::SEG;
-  constexpr int VEC = Geo::VEC;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *base = smem_align1024(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char *wb = base + warp * a.warp_bytes;
   auto stg = [&](int i) { return wb + i * a.stage_bytes; };
-  unsigned char *EB = wb + a.nstages * a.stage_bytes;  // erosion (lowest outside [0, m))
-  unsigned char *DB = EB + a.ebuf_bytes;               // dilation (highest outside)
+  unsigned char *EB = wb + a.nstages * a.stage_bytes;  // erosion at positions j0-(w-1) .. j0+SEG
+  unsigned char *DB = EB + a.ebuf_bytes;               // dilation, same positions
   const WarpAgg<T> agg(DB + a.ebuf_bytes);
   const int w = a.w;
+  const int OFF = Geo::off(w);  // buffer index of position j0
   const int nwb = blockDim.x >> 5;
-  const int64_t gw = blockIdx.x * (int64_t)nwb + warp, nw = (int64_t)gridDim.x * nwb;
-  const int rounds = (SEG + w - 1 + SEG - 1) / SEG;  // pass 1: SEG + w - 1 positions
-
+  const int64_t gw = blockIdx.x * (int64_t)nwb + warp, NW = (int64_t)gridDim.x * nwb;
+  // a contiguous range of segments per warp: the erosion / dilation of the w-1
+  // positions before a segment carry over from the one before it
+  const int64_t s_begin = a.nseg * gw / NW, s_end = a.nseg * (gw + 1) / NW;
+  if (s_begin >= s_end) return;
   auto seg_pos = [&](int64_t sg, int64_t &row, int64_t &j0) {  // nseg < 2^31 (launcher)
     const uint32_t r = (uint32_t)sg / (uint32_t)a.segs_per_row;
     row = r;
     j0 = ((int64_t)sg - (int64_t)r * a.segs_per_row) * SEG;
   };
+  int64_t s_first;
+  {  // warm-up: the segments whose pass 1 feeds the first segment's carried positions
+    int64_t row, j0;
+    seg_pos(s_begin, row, j0);
+    const int64_t wu = (w - 1 + SEG - 1) / SEG, in_row = j0 / SEG;
+    s_first = s_begin - (wu < in_row ? wu : in_row);
+  }
   const int ns = a.nstages;
   for (int k = 0; k + 1 < ns; ++k) {
-    const int64_t sg = gw + k * nw;
-    if (sg < a.nseg) {
+    const int64_t sg = s_first + k;
+    if (sg < s_end) {
       int64_t row, j0;
       seg_pos(sg, row, j0);
       morph_stage<T>(a, stg(k), row, j0, lane);
@@ -186,10 +186,10 @@ __global__ void __launch_bounds__(32 * kMorphWarps) k_morph_fused(MorphArgs a) {
     mcp_async_commit();
   }
   int slot = 0;
-  for (int64_t sg = gw; sg < a.nseg; sg += nw) {
+  for (int64_t sg = s_first; sg < s_end; ++sg) {
     {
-      const int64_t nx = sg + (ns - 1) * nw;
-      if (nx < a.nseg) {
+      const int64_t nx = sg + ns - 1;
+      if (nx < s_end) {
         int64_t row, j0;
         seg_pos(nx, row, j0);
         morph_stage<T>(a, stg(slot + ns - 1 < ns ? slot + ns - 1 : slot - 1), row, j0, lane);
@@ -202,34 +202,37 @@ __global__ void __launch_bounds__(32 * kMorphWarps) k_morph_fused(MorphArgs a) {
     slot = slot + 1 < ns ? slot + 1 : 0;
     int64_t row, j0;
     seg_pos(sg, row, j0);
-    int64_t a0;
-    int p1;
-    morph_base(j0, w, VEC, a0, p1);
-    // ---- pass 1: d (max) and e (min) at positions j0-(w-1) + [0, rounds*SEG)
-    for (int r = 0; r < rounds; ++r) {
+    if (j0 == 0) {  // positions before the row: the identities of pass 2
+      for (int t = lane; t < w - 1; t += 32) {
+        sts_swz<T>(EB, OFF - (w - 1) + t, lowest_value<T>());
+        sts_swz<T>(DB, OFF - (w - 1) + t, highest_value<T>());
+      }
+    }
+    // ---- pass 1: d (max) and e (min) at positions j0 + [0, SEG)
+    {
       T ox[E], on[E];
-      morph_window<T, E, G, false>(X, X, p1 + r * SEG, a.g, agg, lane, ox, on);
-      const int64_t j = j0 - (w - 1) + r * SEG + lane * E;
+      morph_window<T, E, G>(X, 0, a.g, agg, lane, ox, on);
+      const int64_t j = j0 + lane * E;
 #pragma unroll
       for (int k = 0; k < E; ++k) {
-        if (j + k < 0 || j + k >= a.m) {
+        if (j + k >= a.m) {
           ox[k] = highest_value<T>();
           on[k] = lowest_value<T>();
         }
       }
-      sts_swz_chunk<T, E>(DB, r * SEG + lane * E, ox);
-      sts_swz_chunk<T, E>(EB, r * SEG + lane * E, on);
+      sts_swz_chunk<T, E>(DB, OFF + lane * E, ox);
+      sts_swz_chunk<T, E>(EB, OFF + lane * E, on);
     }
     __syncwarp();
-    // ---- pass 2: opening = max over e, closing = min over d
-    {
+    // ---- pass 2: opening = max over e, closing = min over d (outputs j0 + [0, SEG))
+    if (sg >= s_begin) {
       T op[E], cl[E];
       if constexpr (G == 0) {
-        warp_window_small1<T, E, true>(EB, 0, w, lane, op);
-        warp_window_small1<T, E, false>(DB, 0, w, lane, cl);
+        warp_window_small1<T, E, true>(EB, OFF - (w - 1), w, lane, op);
+        warp_window_small1<T, E, false>(DB, OFF - (w - 1), w, lane, cl);
       } else {
-        warp_window_med1<T, E, G, true>(EB, 0, a.g, agg, lane, op);
-        warp_window_med1<T, E, G, false>(DB, 0, a.g, agg, lane, cl);
+        warp_window_med1<T, E, G, true>(EB, OFF - (w - 1), a.g, agg, lane, op);
+        warp_window_med1<T, E, G, false>(DB, OFF - (w - 1), a.g, agg, lane, cl);
       }
       const int64_t i0 = j0 + lane * E;
       const int64_t left = a.n - i0;
@@ -249,7 +252,23 @@ __global__ void __launch_bounds__(32 * kMorphWarps) k_morph_fused(MorphArgs a) {
         }
       }
     }
-    __syncwarp();  // EB / DB and X are rewritten by the next segment
+    // ---- carry: the last w-1 positions move in front of the next segment's
+    if (sg + 1 < s_end && j0 + SEG < a.n) {
+      for (int t0 = 0; t0 < w - 1; t0 += 32) {  // ascending steps: load all, then store
+        const int t = t0 + lane;
+        T ve = T(0), vd = T(0);
+        if (t < w - 1) {
+          ve = lds_one_swz<T>(EB, OFF + SEG - (w - 1) + t);
+          vd = lds_one_swz<T>(DB, OFF + SEG - (w - 1) + t);
+        }
+        __syncwarp();
+        if (t < w - 1) {
+          sts_swz<T>(EB, OFF - (w - 1) + t, ve);
+          sts_swz<T>(DB, OFF - (w - 1) + t, vd);
+        }
+      }
+    }
+    __syncwarp();  // the buffers are rewritten by the next segment
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
 }

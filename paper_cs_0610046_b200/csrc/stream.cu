@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(32 * kStreamWarps) k_stream_fused(StreamArgs a
     const int64_t left = a.c - j0;
     const int cnt = left < SEG ? (int)left : SEG;
     T ox[E], on[E];
-    warp_window_med<T, E, G, false>(X, X, P, a.g, agg, lane, ox, on);
+    warp_window_med<T, E, G>(PairLoader<T>{X}, P, a.g, agg, lane, ox, on);
     const int c0 = lane * E;
     if (c0 < cnt) {
       T *omx = a.out_max ? static_cast<T *>(a.out_max) + row * a.out_ld + j0 + c0 : nullptr;

@@ -114,7 +114,8 @@ def test_binding_raises_without_fallback():
 def test_argfilter_argument_errors(L):
     """N1 entry points: every argument error is reported before any launch."""
     b = ctypes.c_size_t(0)
-    assert L.maxmin_argfilter_workspace_bytes(8, 1, 1000, 10, ctypes.byref(b)) == 0 and b.value > 32 * 990
+    assert L.maxmin_argfilter_workspace_bytes(8, 1, 1000, 10, ctypes.byref(b)) == 0 and b.value == 0  # fused
+    assert L.maxmin_argfilter_workspace_bytes(8, 1, 5000, 2000, ctypes.byref(b)) == 0 and b.value > 32 * 3000
     assert L.maxmin_argfilter_workspace_bytes(9, 1, 1000, 10, ctypes.byref(b)) == 10  # f64: unsupported
     assert L.maxmin_argfilter_workspace_bytes(8, 1, 10, 0, ctypes.byref(b)) == 3
     assert L.maxmin_argfilter_workspace_bytes(8, 1, 10, 11, ctypes.byref(b)) == 4
@@ -124,7 +125,7 @@ def test_argfilter_argument_errors(L):
     assert f(8, None, 1, 100, 100, 10, P + (1 << 24), None, None, None, 91, P + (1 << 26), 1 << 20, None) == 1
     assert f(8, P, 1, 100, 100, 10, None, None, None, None, 91, P + (1 << 26), 1 << 20, None) == 1
     assert f(8, P, 1, 100, 100, 10, None, None, P + (1 << 24) + 4, None, 91, P + (1 << 26), 1 << 20, None) == 6
-    assert f(8, P, 1, 100, 100, 10, None, None, P + (1 << 24), None, 91, None, 0, None) == 8
+    assert f(8, P, 1, 5000, 5000, 2000, None, None, P + (1 << 24), None, 3001, None, 0, None) == 8
     assert f(8, P, 1, 100, 100, 10, None, None, P + 8, None, 91, P + (1 << 26), 1 << 20, None) == 7
     assert f(9, P, 1, 100, 100, 10, None, None, P + (1 << 24), None, 91, P + (1 << 26), 1 << 20, None) == 10
 

@@ -340,7 +340,7 @@ def test_argfilter_every_dtype(cuda_device, dtype):
     """Values and earliest positions of max/min vs the definition, with ties
     (small alphabets) and every kernel path of the key filters."""
     n = 20_003
-    for k, w in enumerate([1, 2, 3, 8, 9, 100, 1000, 5000, 9000]):
+    for k, w in enumerate([1, 2, 3, 7, 8, 9, 16, 17, 100, 129, 1000, 1025, 1026, 5000, 9000]):
         a = synth.random_values(dtype, n, seed=2000 + k, alphabet=(4 if k % 2 else None))
         x = torch.from_numpy(a).to(dev())
         mx, mn, ax, an = mm.maxmin_argfilter_1d(x, w)
@@ -366,6 +366,38 @@ def test_argfilter_brute_and_batched(cuda_device):
     _, _, ax, an = mm.maxmin_argfilter_batched(x, 77, want_min=False, values=False)
     assert an is None
     assert_same(ax[1], oracle.arg_brute(a[1], 77)[2])
+
+
+def test_argfilter_unaligned_rows_and_outputs(cuda_device):
+    """Odd input pitch and odd output pitch through the C ABI: the fused kernel's
+    element-wise staging and scalar stores."""
+    import ctypes
+
+    batch, n, ld, w = 5, 3001, 3003, 129
+    a = synth.random_values(np.int16, batch * ld, seed=77, alphabet=5).reshape(batch, ld)
+    x = torch.from_numpy(a).to(dev())
+    m = n - w + 1
+    out_ld = m + 1
+    ox = torch.empty(batch * out_ld + 1, dtype=torch.int16, device=dev())[1:]  # 2-B aligned only
+    on = torch.empty_like(ox)
+    ax = torch.empty(batch * out_ld, dtype=torch.int64, device=dev())
+    an = torch.empty_like(ax)
+    L = mm._lib.lib()
+    vp = ctypes.c_void_p
+    need = mm.maxmin_argfilter_workspace_bytes(torch.int16, batch, n, w)
+    ws = torch.empty(max(need, 16), dtype=torch.uint8, device=dev())
+    mm._lib.check(L.maxmin_argfilter_batched(mm.dtype_code(torch.int16), vp(x.data_ptr()), batch, n, ld, w,
+                                             vp(ox.data_ptr()), vp(on.data_ptr()), vp(ax.data_ptr()),
+                                             vp(an.data_ptr()), out_ld, vp(ws.data_ptr()), ws.numel(),
+                                             vp(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    for r in range(batch):
+        ex, en, eax, ean = oracle.arg_brute(a[r, :n], w)
+        sl = slice(r * out_ld, r * out_ld + m)
+        assert_same(ox[sl], ex, f"row {r} max")
+        assert_same(on[sl], en, f"row {r} min")
+        assert_same(ax[sl], eax, f"row {r} argmax")
+        assert_same(an[sl], ean, f"row {r} argmin")
 
 
 def test_argfilter_c2_full_size(cuda_device):
