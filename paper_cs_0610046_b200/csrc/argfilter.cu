@@ -131,6 +131,9 @@ size_t argfilter_workspace(int64_t batch, int64_t n, int64_t w) {
 template <typename S>
 int launch_arg_fused(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w, void *out_max, void *out_min,
                      int64_t *arg_max, int64_t *arg_min, int64_t out_ld, cudaStream_t s);
+template <typename S>
+int launch_arg_medium(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w, void *out_max,
+                      void *out_min, int64_t *arg_max, int64_t *arg_min, int64_t out_ld, cudaStream_t s);
 
 template <typename T>
 int launch_argfilter(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w, void *out_max,
@@ -139,7 +142,9 @@ int launch_argfilter(const void *in, int64_t batch, int64_t n, int64_t in_ld, in
   static_assert(sizeof(T) <= 4, "keys hold a 32-bit order code and a 32-bit position");
   if (batch == 0) return kOK;
   {
-    const int rc = launch_arg_fused<T>(in, batch, n, in_ld, w, out_max, out_min, arg_max, arg_min, out_ld, s);
+    int rc = launch_arg_medium<T>(in, batch, n, in_ld, w, out_max, out_min, arg_max, arg_min, out_ld, s);
+    if (rc != kErrUnsupported) return rc;
+    rc = launch_arg_fused<T>(in, batch, n, in_ld, w, out_max, out_min, arg_max, arg_min, out_ld, s);
     if (rc != kErrUnsupported) return rc;
   }
   const ArgLayout L = arg_layout(batch, n, w);
@@ -385,6 +390,150 @@ int launch_arg_g(ArgArgs a, cudaStream_t s) {
   const int64_t cap = (int64_t)sm_count() * per_sm;
   k_arg_fused<S, G><<<(int)(want < cap ? want : cap), 32 * best_nw, smem, s>>>(a);
   return note_cuda(cudaGetLastError());
+}
+
+// ------------------------------------------- CTA path: k1d_medium on keys
+// 8 < w <= kHaloMax+1: the library's medium kernel (TMA tiles of 2048 windows,
+// far-block aggregates carried across tiles) filters the keys, built from the
+// staged values inside its loads (ArgSrc), and the epilogue decodes them.
+template <typename V>
+struct ArgSrc {
+  using S = V;  // staged element type (k1d_medium's Src::S)
+  static constexpr bool TWO = true;
+  template <int E>
+  __device__ __forceinline__ static void keys(const S (&v)[E], int64_t p0, uint64_t (&ya)[E], uint64_t (&yb)[E]) {
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const uint64_t o = (uint64_t)ord32<S>(v[k]) << 32;
+      const uint32_t i = (uint32_t)p0 + (uint32_t)k;
+      ya[k] = o | (0xffffffffu - i);
+      yb[k] = o | i;
+    }
+  }
+  template <int E>
+  __device__ __forceinline__ static void load(const unsigned char *X, int pos, int64_t u0, uint64_t (&ya)[E],
+                                              uint64_t (&yb)[E]) {
+    S v[E];
+    lds_swz<S, E>(X, pos, v);
+    keys<E>(v, u0 + pos, ya, yb);
+  }
+  template <int E>
+  __device__ __forceinline__ static void load_aligned(const unsigned char *X, int pos, int64_t u0, uint64_t (&ya)[E],
+                                                      uint64_t (&yb)[E]) {
+    S v[E];
+    lds_swz<S, E>(X, pos, v);  // E*sizeof(S) may be < 16 B: the general read
+    keys<E>(v, u0 + pos, ya, yb);
+  }
+};
+template <typename S>
+struct ArgEpi {
+  S *out_max, *out_min;
+  int64_t *arg_max, *arg_min;
+  int64_t out_ld;
+  int vec;  // every output row 16-B aligned
+  template <typename T, int E>
+  __device__ __forceinline__ void operator()(const Rows &p, int64_t row, int64_t j0, int cnt, const T (&ox)[E],
+                                             const T (&on)[E]) const {
+    if (cnt <= 0) return;
+    S vx[E], vn[E];
+    int64_t ix[E], in_[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      vx[k] = unord32<S>((uint32_t)(ox[k] >> 32));
+      ix[k] = (int64_t)(0xffffffffu - (uint32_t)ox[k]);
+      vn[k] = unord32<S>((uint32_t)(on[k] >> 32));
+      in_[k] = (int64_t)(uint32_t)on[k];
+    }
+    const int64_t o = row * out_ld + j0;
+    S *omx = out_max ? out_max + o : nullptr;
+    S *omn = out_min ? out_min + o : nullptr;
+    int64_t *oax = arg_max ? arg_max + o : nullptr;
+    int64_t *oan = arg_min ? arg_min + o : nullptr;
+    if (cnt >= E && vec) {
+      if constexpr ((E * sizeof(S)) % 16 == 0) {
+        if (omx) store_chunk<S, E>(omx, vx);
+        if (omn) store_chunk<S, E>(omn, vn);
+      } else {
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+          if (omx) omx[k] = vx[k];
+          if (omn) omn[k] = vn[k];
+        }
+      }
+      if (oax) store_chunk<int64_t, E>(oax, ix);
+      if (oan) store_chunk<int64_t, E>(oan, in_);
+    } else {
+#pragma unroll
+      for (int k = 0; k < E; ++k)
+        if (k < cnt) {
+          if (omx) omx[k] = vx[k];
+          if (omn) omn[k] = vn[k];
+          if (oax) oax[k] = ix[k];
+          if (oan) oan[k] = in_[k];
+        }
+    }
+  }
+};
+
+template <typename S, int G>
+int launch_arg_medium_g(const Rows &p, const TmaMaps &maps, const ArgEpi<S> &epi, cudaStream_t s) {
+  auto kern = k1d_medium<uint64_t, G, ArgEpi<S>, ArgSrc<S>>;
+  static size_t attr = 0;
+  const MedGeom g = medium_geom<uint64_t>(p.w, G);
+  const size_t smem = MedLayoutS<uint64_t, S>::bytes(p.w, g.ring);
+  int rc = set_smem(kern, smem, attr);
+  if (rc) return rc;
+  int grid = 0;
+  rc = occupancy_grid(kern, smem, p.ntiles, grid);
+  if (rc) return rc;
+  kern<<<grid, NT, smem, s>>>(p, g, maps, epi);
+  return note_cuda(cudaGetLastError());
+}
+
+template <typename S>
+int launch_arg_medium(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w, void *out_max,
+                      void *out_min, int64_t *arg_max, int64_t *arg_min, int64_t out_ld, cudaStream_t s) {
+  if (w <= Chunk<uint64_t>::E || w > kHaloMax + 1) return kErrUnsupported;
+  if ((reinterpret_cast<uintptr_t>(in) % 16) != 0 || (batch > 1 && (in_ld * (int64_t)sizeof(S)) % 16 != 0))
+    return kErrUnsupported;  // TMA rows
+  Rows p;
+  std::memset(&p, 0, sizeof(p));
+  p.in = in;
+  p.n = n;
+  p.w = w;
+  p.m = n - w + 1;
+  p.in_ld = in_ld;
+  p.out_ld = out_ld;
+  p.batch = batch;
+  p.tiles_per_row = (p.m + Geo1D<uint64_t>::TILE - 1) / Geo1D<uint64_t>::TILE;
+  p.ntiles = batch * p.tiles_per_row;
+  TmaMaps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  const int64_t full_rows = n / Rowing<S>::RW;
+  p.has_map = full_rows > 0 ? 1 : 0;
+  if (p.has_map) {
+    int rc = encode_rows_map(&maps.small, in, (int)sizeof(S), full_rows, batch, in_ld * (int64_t)sizeof(S));
+    if (rc) return rc;
+    rc = encode_rows_map(&maps.big, in, (int)sizeof(S), full_rows, batch, in_ld * (int64_t)sizeof(S), kBigRows);
+    if (rc) return rc;
+  }
+  ArgEpi<S> epi;
+  epi.out_max = static_cast<S *>(out_max);
+  epi.out_min = static_cast<S *>(out_min);
+  epi.arg_max = arg_max;
+  epi.arg_min = arg_min;
+  epi.out_ld = out_ld;
+  auto al = [](const void *q) { return q == nullptr || reinterpret_cast<uintptr_t>(q) % 16 == 0; };
+  epi.vec = (al(out_max) && al(out_min) && al(arg_max) && al(arg_min) && (out_ld * 8) % 16 == 0 &&
+             (out_ld * (int64_t)sizeof(S)) % 16 == 0) ? 1 : 0;
+  switch (medium_G<uint64_t>(w)) {
+    case 1: return launch_arg_medium_g<S, 1>(p, maps, epi, s);
+    case 2: return launch_arg_medium_g<S, 2>(p, maps, epi, s);
+    case 4: return launch_arg_medium_g<S, 4>(p, maps, epi, s);
+    case 8: return launch_arg_medium_g<S, 8>(p, maps, epi, s);
+    case 16: return launch_arg_medium_g<S, 16>(p, maps, epi, s);
+    default: return launch_arg_medium_g<S, 32>(p, maps, epi, s);
+  }
 }
 
 // kErrUnsupported when the fused path does not apply (the caller composes)

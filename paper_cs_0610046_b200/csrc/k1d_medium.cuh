@@ -77,17 +77,58 @@ __device__ __forceinline__ void grp_scan_down(T &vx, T &vn, int gl) {
   }
 }
 
-template <typename T, int G, class Epi = StoreEpi>
+// Source of the values a tile is filtered on.  SameSrc: the staged elements
+// themselves (both chains read them).  Other sources (argfilter.cu's ArgSrc)
+// stage elements of another type S and build the max chain's and the min
+// chain's values from them and their row positions inside the loads.
+template <typename T>
+struct SameSrc {
+  using S = T;
+  static constexpr bool TWO = false;
+  template <int E>
+  __device__ __forceinline__ static void load(const unsigned char *X, int pos, int64_t, T (&ya)[E], T (&yb)[E]) {
+    lds_swz<T, E>(X, pos, ya);
+#pragma unroll
+    for (int k = 0; k < E; ++k) yb[k] = ya[k];
+  }
+  template <int E>
+  __device__ __forceinline__ static void load_aligned(const unsigned char *X, int pos, int64_t, T (&ya)[E],
+                                                      T (&yb)[E]) {
+    lds_swz_aligned<T, E>(X, pos, ya);
+#pragma unroll
+    for (int k = 0; k < E; ++k) yb[k] = ya[k];
+  }
+};
+
+// shared-memory layout for a tile of T-windows staged as S elements
+template <typename T, typename S>
+struct MedLayoutS {
+  static constexpr int TILE = MedLayout<T>::TILE;
+  static constexpr int RW = Rowing<S>::RW;
+  __host__ __device__ static int rows(int64_t w) {
+    int r = (int)((TILE + w - 1 + 16 + RW - 1) / RW);
+    return (r + kBoxRows - 1) / kBoxRows * kBoxRows;
+  }
+  __host__ __device__ static size_t stage_bytes(int64_t w) { return (size_t)rows(w) * 128; }
+  __host__ __device__ static size_t bytes(int64_t w, int ring) {
+    return 1024 + 2 * stage_bytes(w) + 4 * sizeof(T) * (size_t)ring + 64;
+  }
+};
+
+template <typename T, int G, class Epi = StoreEpi, class Src = SameSrc<T>>
 __global__ void __launch_bounds__(NT, 2)
     k1d_medium(Rows p, MedGeom g, const __grid_constant__ TmaMaps maps, Epi epi = Epi()) {
   using Lay = MedLayout<T>;
+  using S = typename Src::S;
+  using LayS = MedLayoutS<T, S>;
+  constexpr bool TWO = Src::TWO;
   constexpr int E = Lay::E;
   constexpr int TILE = Lay::TILE;
   constexpr int B = E * G;
   constexpr int NG = NT / G;  // groups per tile
   const int RMASK = g.ring - 1;
   const int w = (int)p.w;
-  const size_t SB = Lay::stage_bytes(w);
+  const size_t SB = LayS::stage_bytes(w);
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *base = smem_align1024(smem_raw);
@@ -122,7 +163,7 @@ __global__ void __launch_bounds__(NT, 2)
   }
   __syncthreads();
   if (tid == 0 && t_begin < t_end)
-    stage_tile2<T>(p, &maps, stg(0), cur.row, cur.u0, cur.tout(p) + w - 1, &bars[0]);
+    stage_tile2<S>(p, &maps, stg(0), cur.row, cur.u0, cur.tout(p) + w - 1, &bars[0]);
 
   // H contribution of a chunk y (block-relative chunk gl) given its local max
   auto h_part = [&](const T (&y)[E], T ax, T an, T bl, T &hx, T &hn) {
@@ -146,12 +187,12 @@ __global__ void __launch_bounds__(NT, 2)
     const unsigned char *X = stg(st);
     nxt.advance(p);
     if (tid == 0 && t + 1 < t_end)  // prefetch the next tile into the other stage
-      stage_tile2<T>(p, &maps, stg(st ^ 1), nxt.row, nxt.u0, nxt.tout(p) + w - 1, &bars[st ^ 1]);
+      stage_tile2<S>(p, &maps, stg(st ^ 1), nxt.row, nxt.u0, nxt.tout(p) + w - 1, &bars[st ^ 1]);
     const int64_t row = cur.row, u0 = cur.u0;
     const int tout = cur.tout(p);
     const int64_t ab0 = u0 / B;  // far block index (within the row) of group 0
     mbar_wait(&bars[st], (it >> 1) & 1);
-    if (patch_tail<T>(p, stg(st), row, u0, tout + w - 1, tid)) __syncthreads();
+    if (patch_tail<S>(p, stg(st), row, u0, tout + w - 1, tid)) __syncthreads();
 
     // ------------------------------------------------- far chunk: prefix
     // ux/un end up as max(P, S) per element: local prefix of the far chunk
@@ -159,24 +200,27 @@ __global__ void __launch_bounds__(NT, 2)
     T ux[E], un[E];
     T cx, cn;
     {
-      T y[E];
-      lds_swz<T, E>(X, tid * E + w - 1, y);
-      ux[0] = un[0] = y[0];
+      T ya[E], yb[E];
+      Src::template load<E>(X, tid * E + w - 1, u0, ya, yb);
+      ux[0] = ya[0];
+      un[0] = yb[0];
 #pragma unroll
       for (int k = 1; k < E; ++k) {
-        ux[k] = Ord<T>::mx(ux[k - 1], y[k]);
-        un[k] = Ord<T>::mn(un[k - 1], y[k]);
+        ux[k] = Ord<T>::mx(ux[k - 1], ya[k]);
+        un[k] = Ord<T>::mn(un[k - 1], yb[k]);
       }
-      T hx, hn;
-      h_part(y, ux[E - 1], un[E - 1], __shfl_sync(0xffffffffu, y[E - 1], glast), hx, hn);
+      T hx, hn, tx, tn;
+      h_part(ya, ux[E - 1], un[E - 1], __shfl_sync(0xffffffffu, ya[E - 1], glast), hx, tn);
+      if (TWO) h_part(yb, ux[E - 1], un[E - 1], __shfl_sync(0xffffffffu, yb[E - 1], glast), tx, hn);
+      else hn = tn;
       grp_reduce<T, G>(hx, hn);
       T ax = ux[E - 1], an = un[E - 1];  // group-inclusive prefix of chunk maxima
       grp_scan_up<T, G>(ax, an, gl);
       cx = shfl_up(ax, 1);
       cn = shfl_up(an, 1);
       if (gl == 0) {  // nothing before: an element inside every window
-        cx = y[0];
-        cn = y[0];
+        cx = ya[0];
+        cn = yb[0];
       }
       if (gl == G - 1) {  // publish far block aggregates G_g, H_g
         const int ri = (int)((ab0 + grp) & RMASK);
@@ -189,15 +233,15 @@ __global__ void __launch_bounds__(NT, 2)
 
     // ------------------------------------------------ near chunk: suffix
     {
-      T x[E];
-      lds_swz_aligned<T, E>(X, tid * E, x);
-      T sx = x[E - 1], sn = x[E - 1];
+      T xa[E], xb[E];
+      Src::template load_aligned<E>(X, tid * E, u0, xa, xb);
+      T sx = xa[E - 1], sn = xb[E - 1];
       ux[E - 1] = Ord<T>::mx(ux[E - 1], sx);
       un[E - 1] = Ord<T>::mn(un[E - 1], sn);
 #pragma unroll
       for (int k = E - 2; k >= 0; --k) {
-        sx = Ord<T>::mx(sx, x[k]);
-        sn = Ord<T>::mn(sn, x[k]);
+        sx = Ord<T>::mx(sx, xa[k]);
+        sn = Ord<T>::mn(sn, xb[k]);
         ux[k] = Ord<T>::mx(ux[k], sx);
         un[k] = Ord<T>::mn(un[k], sn);
       }
@@ -205,8 +249,8 @@ __global__ void __launch_bounds__(NT, 2)
       grp_scan_down<T, G>(bx, bn, gl);
       T ex = shfl_down(bx, 1), en = shfl_down(bn, 1);
       if (gl == G - 1) {  // nothing after: an element inside every window of the chunk
-        ex = x[E - 1];
-        en = x[E - 1];
+        ex = xa[E - 1];
+        en = xb[E - 1];
       }
       cx = Ord<T>::mx(cx, ex);
       cn = Ord<T>::mn(cn, en);
@@ -222,16 +266,18 @@ __global__ void __launch_bounds__(NT, 2)
         const int vcc = vc < nv ? vc : nv - 1;
         const int gv = vcc / G;  // 0 .. V-1  <->  g' = gv - V
         const int pos = (gv - g.V) * B + w - 1 + gl * E;
-        T y[E];
-        lds_swz<T, E>(X, pos, y);
-        T ax = y[0], an = y[0];
+        T ya[E], yb[E];
+        Src::template load<E>(X, pos, u0, ya, yb);
+        T ax = ya[0], an = yb[0];
 #pragma unroll
         for (int k = 1; k < E; ++k) {
-          ax = Ord<T>::mx(ax, y[k]);
-          an = Ord<T>::mn(an, y[k]);
+          ax = Ord<T>::mx(ax, ya[k]);
+          an = Ord<T>::mn(an, yb[k]);
         }
-        T hx, hn;
-        h_part(y, ax, an, __shfl_sync(0xffffffffu, y[E - 1], glast), hx, hn);
+        T hx, hn, tx, tn;
+        h_part(ya, ax, an, __shfl_sync(0xffffffffu, ya[E - 1], glast), hx, tn);
+        if (TWO) h_part(yb, ax, an, __shfl_sync(0xffffffffu, yb[E - 1], glast), tx, hn);
+        else hn = tn;
         grp_reduce<T, G>(ax, an);
         grp_reduce<T, G>(hx, hn);
         if (vc < nv && gl == 0) {

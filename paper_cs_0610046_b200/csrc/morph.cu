@@ -142,8 +142,11 @@ __device__ __forceinline__ void morph_window(const unsigned char *X, int pos0, c
     warp_window_med<T, E, G>(PairLoader<T>{X}, pos0, g, agg, lane, ox, on);
 }
 
+#ifndef MM_MORPH_MINB
+#define MM_MORPH_MINB 1
+#endif
 template <typename T, int G>
-__global__ void __launch_bounds__(32 * kMorphWarps) k_morph_fused(MorphArgs a) {
+__global__ void __launch_bounds__(32 * kMorphWarps, MM_MORPH_MINB) k_morph_fused(MorphArgs a) {
   using Geo = MorphGeo<T>;
   constexpr int E = Geo::E;
   constexpr int SEG = Geo::SEG;
