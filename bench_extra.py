@@ -322,7 +322,9 @@ def run_extra(args, rank, world, local):
             "config": {"workload": name, "l2": l2,
                        "parallelism": f"item sharding, dp{world}" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src},
+                         "frac": achieved / peak, "traffic": bench.ncu_traffic(cfg, windows[0]),
+                         "traffic_unit": "dram bytes per launch of the dominant kernel (profiles/ncu_traffic.json)",
+                         "peak_source": peak_src},
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": steps * {"N3": 3, "N2": 16}.get(cfg, 1), "clocks": clk,
             "parity": {"bit_exact": parity},

@@ -4,7 +4,7 @@ cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem,power.draw --format=csv > gpurun_out/smi.txt 2>&1
 timeout 600 python bench.py > gpurun_out/bench_c2.log 2>&1; echo "rc=$?" >> gpurun_out/bench_c2.log
-for c in C1 C3 C4 C5; do
+for c in C1 C3 C4 C5 N1 N2 N3 N4; do
   timeout 600 python bench.py --config $c --steps 20 > gpurun_out/bench_$c.log 2>&1; echo "rc=$?" >> gpurun_out/bench_$c.log
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "rc=$?" >> gpurun_out/bench_ref.log
@@ -16,4 +16,10 @@ for spec in "C2 3 k1d" "C2 32 k1d" "C2 1024 k1d" "C2 65536 k1d" "C3 129 k1d" "C4
   timeout 200 python tools/prof_one.py --config $1 --w $2 --reps 2 > gpurun_out/plain_$1_$2.log 2>&1 && \
   timeout 400 ncu --set full --clock-control none --import-source on -k regex:$3 -s 1 -c 1 -o gpurun_out/prof_$1_w$2 -f \
     python tools/prof_one.py --config $1 --w $2 --reps 2 > gpurun_out/ncu_$1_$2.log 2>&1
+done
+for spec in "N1 k1d_medium" "N2 k_stream_fused" "N3 k1d_medium" "N4 k_morph_fused"; do
+  set -- $spec
+  timeout 200 python tools/prof_next.py --op $1 > gpurun_out/plain_$1.log 2>&1 && \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$2 -s 3 -c 1 -o gpurun_out/prof_$1 -f \
+    python tools/prof_next.py --op $1 > gpurun_out/ncu_$1.log 2>&1
 done
