@@ -356,58 +356,175 @@ int launch_morph(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_
 }
 
 // ------------------------------------------------------------------- 2-D
+// The identity frames of the two padded buffers: every element outside rows
+// [r0, r1) x columns [c0, c1).  One warp per (image, padded row): whole rows
+// above and below the interior, the left and right margins beside it.
 template <typename T>
 __global__ void k_morph_frame(T *pe, T *pd, int64_t batch, int64_t PR, int64_t PC, int64_t ld, int64_t bs,
                               int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
-  // every element of the padded buffers outside rows [r0, r1) x columns [c0, c1)
-  const int64_t total = batch * PR * PC;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = t / (PR * PC), rc = t - b * PR * PC, r = rc / PC, c = rc - r * PC;
-    if (r >= r0 && r < r1 && c >= c0 && c < c1) continue;
-    pe[b * bs + r * ld + c] = lowest_value<T>();
-    pd[b * bs + r * ld + c] = highest_value<T>();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const T lo = lowest_value<T>(), hi = highest_value<T>();
+  for (int64_t it = warp; it < batch * PR; it += nw) {
+    const int64_t b = it / PR, r = it - b * PR;
+    T *er = pe + b * bs + r * ld;
+    T *dr = pd + b * bs + r * ld;
+    if (r < r0 || r >= r1) {
+      for (int64_t c = lane; c < PC; c += 32) {
+        er[c] = lo;
+        dr[c] = hi;
+      }
+    } else {
+      for (int64_t c = lane; c < c0; c += 32) {
+        er[c] = lo;
+        dr[c] = hi;
+      }
+      for (int64_t c = c1 + lane; c < PC; c += 32) {
+        er[c] = lo;
+        dr[c] = hi;
+      }
+    }
+  }
+}
+
+// dst[b][r][c] = src[b][r][c] for an R x C block of bytes, twice (the erosion
+// and the dilation): source rows 16-B aligned, destination rows misaligned by
+// the same D bytes (the interior of a padded frame).  One warp per (image, row)
+// walks the row in 512-B steps; lane l writes destination 16-B unit u, whose
+// bytes are source bytes [16u-D, 16u-D+16): the tail of source unit u-1 (the
+// previous lane's, via a shuffle) and the head of unit u, joined with funnel
+// shifts.  The first and last units of a row are partial: byte stores.
+__device__ __forceinline__ void place_row(const uint8_t *__restrict__ sr, uint8_t *dr, int64_t C, int D, int lane) {
+  uint8_t *A = dr - D;  // 16-B aligned
+  const int64_t nu = (D + C + 15) / 16;
+  const int P = 16 - D;  // start of the wanted bytes in [unit u-1 | unit u]
+  const int wi = P >> 2, sh = (P & 3) * 8;
+  uint4 carry = make_uint4(0, 0, 0, 0);
+  for (int64_t ub = 0; ub < nu; ub += 32) {
+    const int64_t u = ub + lane;
+    uint4 cur = make_uint4(0, 0, 0, 0);
+    if (u * 16 < C) cur = *reinterpret_cast<const uint4 *>(sr + u * 16);
+    uint4 prev;
+    prev.x = __shfl_up_sync(0xffffffffu, cur.x, 1);
+    prev.y = __shfl_up_sync(0xffffffffu, cur.y, 1);
+    prev.z = __shfl_up_sync(0xffffffffu, cur.z, 1);
+    prev.w = __shfl_up_sync(0xffffffffu, cur.w, 1);
+    if (lane == 0) prev = carry;
+    carry.x = __shfl_sync(0xffffffffu, cur.x, 31);
+    carry.y = __shfl_sync(0xffffffffu, cur.y, 31);
+    carry.z = __shfl_sync(0xffffffffu, cur.z, 31);
+    carry.w = __shfl_sync(0xffffffffu, cur.w, 31);
+    if (u >= nu) continue;
+    const uint32_t W[9] = {prev.x, prev.y, prev.z, prev.w, cur.x, cur.y, cur.z, cur.w, 0u};
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t lo = 0, hi = 0;
+#pragma unroll
+      for (int q = 0; q < 5; ++q)  // W[wi + k], W[wi + k + 1] with a uniform wi in [0, 4]
+        if (q == wi) {
+          lo = W[q + k];
+          hi = W[q + k + 1];
+        }
+      o[k] = __funnelshift_r(lo, hi, sh);
+    }
+    const int64_t t0 = u * 16;  // destination bytes [t0, t0+16) relative to A; valid [D, D+C)
+    if (t0 >= D && t0 + 16 <= D + C) {
+      *reinterpret_cast<uint4 *>(A + t0) = make_uint4(o[0], o[1], o[2], o[3]);
+    } else {
+      const uint8_t *ob = reinterpret_cast<const uint8_t *>(o);
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (t0 + k >= D && t0 + k < D + C) A[t0 + k] = ob[k];
+    }
+  }
+}
+
+__global__ void k_morph_place_u8(const uint8_t *__restrict__ se, const uint8_t *__restrict__ sd, int64_t sld,
+                                 int64_t sbs, uint8_t *de, uint8_t *dd, int64_t dld, int64_t dbs, int64_t batch,
+                                 int64_t R, int64_t C, int D) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t it = warp; it < 2 * batch * R; it += nw) {
+    const int which = it >= batch * R ? 1 : 0;
+    const int64_t k = it - which * batch * R;
+    const int64_t b = k / R, r = k - b * R;
+    place_row((which ? sd : se) + b * sbs + r * sld, (which ? dd : de) + b * dbs + r * dld, C, D, lane);
   }
 }
 
 template <typename T>
+struct Morph2DLayout {  // workspace: [padded e | padded d | (1-byte types) aligned e | aligned d]
+  int64_t PR, PC, ld, bs;  // padded frames
+  int64_t R, C, eld, ebs;  // aligned valid-region buffers
+  size_t frame, valid, total;
+  Morph2DLayout(int64_t batch, int64_t rows, int64_t cols, int64_t w_row, int64_t w_col) {
+    constexpr int VEC = 16 / (int)sizeof(T);
+    auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+    PR = rows + w_col - 1;
+    PC = cols + w_row - 1;
+    ld = (PC + VEC - 1) / VEC * VEC;
+    bs = PR * ld;
+    frame = up((size_t)batch * bs * sizeof(T));
+    R = rows - w_col + 1;
+    C = cols - w_row + 1;
+    eld = (C + VEC - 1) / VEC * VEC;
+    ebs = R * eld;
+    valid = sizeof(T) == 1 ? up((size_t)batch * ebs) : 0;
+    total = 2 * frame + 2 * valid;
+  }
+};
+
+template <typename T>
 size_t morph_2d_workspace(int64_t batch, int64_t rows, int64_t cols, int64_t w_row, int64_t w_col) {
-  constexpr int VEC = 16 / (int)sizeof(T);
-  const int64_t PR = rows + w_col - 1, PC = cols + w_row - 1;
-  const int64_t ld = (PC + VEC - 1) / VEC * VEC;
-  const size_t one = ((size_t)batch * PR * ld * sizeof(T) + 255) & ~size_t(255);
-  return 2 * one;
+  return Morph2DLayout<T>(batch, rows, cols, w_row, w_col).total;
 }
 
 template <typename T>
 int launch_morph_2d(const void *in, int64_t batch, int64_t rows, int64_t cols, int64_t in_ld, int64_t in_bstride,
                     int64_t w_row, int64_t w_col, void *out_open, void *out_close, int64_t out_ld,
                     int64_t out_bstride, void *ws, cudaStream_t s) {
-  constexpr int VEC = 16 / (int)sizeof(T);
   if (batch == 0) return kOK;
-  const int64_t PR = rows + w_col - 1, PC = cols + w_row - 1;
-  const int64_t ld = (PC + VEC - 1) / VEC * VEC;
-  const int64_t bs = PR * ld;
-  const size_t one = ((size_t)batch * PR * ld * sizeof(T) + 255) & ~size_t(255);
-  T *pe = static_cast<T *>(ws);
-  T *pd = reinterpret_cast<T *>(static_cast<char *>(ws) + one);
+  const Morph2DLayout<T> L(batch, rows, cols, w_row, w_col);
+  char *base = static_cast<char *>(ws);
+  T *pe = reinterpret_cast<T *>(base);
+  T *pd = reinterpret_cast<T *>(base + L.frame);
   {
-    const int64_t total = batch * PR * PC;
-    const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 8);
-    k_morph_frame<T><<<(int)(blocks > 0 ? blocks : 1), 256, 0, s>>>(pe, pd, batch, PR, PC, ld, bs, w_col - 1,
-                                                                     w_col - 1 + rows - w_col + 1, w_row - 1,
-                                                                     w_row - 1 + cols - w_row + 1);
+    const int64_t items = batch * L.PR;
+    const int64_t blocks = std::min<int64_t>((items + 7) / 8, (int64_t)sm_count() * 8);
+    k_morph_frame<T><<<(int)(blocks > 0 ? blocks : 1), 256, 0, s>>>(pe, pd, batch, L.PR, L.PC, L.ld, L.bs, w_col - 1,
+                                                                     w_col - 1 + L.R, w_row - 1, w_row - 1 + L.C);
     int rc = note_cuda(cudaGetLastError());
     if (rc) return rc;
   }
-  // e (min) and d (max) of the valid region into the frames' interiors
-  const int64_t off = (w_col - 1) * ld + (w_row - 1);
-  int rc = launch_2d<T>(in, batch, rows, cols, in_ld, in_bstride, w_row, w_col, pd + off, pe + off, ld, bs, s);
+  const int64_t off = (w_col - 1) * L.ld + (w_row - 1);
+  int rc;
+  if (sizeof(T) == 1) {
+    // the packed byte kernel writes 4-B aligned rows only: e and d go to aligned
+    // buffers first, then into the frames' (unaligned) interiors
+    T *ve = reinterpret_cast<T *>(base + 2 * L.frame);
+    T *vd = reinterpret_cast<T *>(base + 2 * L.frame + L.valid);
+    rc = launch_2d<T>(in, batch, rows, cols, in_ld, in_bstride, w_row, w_col, vd, ve, L.eld, L.ebs, s);
+    if (rc) return rc;
+    const int64_t items = 2 * batch * L.R;
+    const int64_t blocks = std::min<int64_t>((items + 7) / 8, (int64_t)sm_count() * 16);
+    const int D = (int)(reinterpret_cast<uintptr_t>(pe + off) & 15);  // same for every row (ld % 16 == 0)
+    k_morph_place_u8<<<(int)(blocks > 0 ? blocks : 1), 256, 0, s>>>(
+        reinterpret_cast<const uint8_t *>(ve), reinterpret_cast<const uint8_t *>(vd), L.eld, L.ebs,
+        reinterpret_cast<uint8_t *>(pe + off), reinterpret_cast<uint8_t *>(pd + off), L.ld, L.bs, batch, L.R, L.C, D);
+    rc = note_cuda(cudaGetLastError());
+  } else {  // the generic 2-D kernel stores at any element alignment
+    rc = launch_2d<T>(in, batch, rows, cols, in_ld, in_bstride, w_row, w_col, pd + off, pe + off, L.ld, L.bs, s);
+  }
   if (rc) return rc;
   if (out_open) {
-    rc = launch_2d<T>(pe, batch, PR, PC, ld, bs, w_row, w_col, out_open, nullptr, out_ld, out_bstride, s);
+    rc = launch_2d<T>(pe, batch, L.PR, L.PC, L.ld, L.bs, w_row, w_col, out_open, nullptr, out_ld, out_bstride, s);
     if (rc) return rc;
   }
-  if (out_close) rc = launch_2d<T>(pd, batch, PR, PC, ld, bs, w_row, w_col, nullptr, out_close, out_ld, out_bstride, s);
+  if (out_close)
+    rc = launch_2d<T>(pd, batch, L.PR, L.PC, L.ld, L.bs, w_row, w_col, nullptr, out_close, out_ld, out_bstride, s);
   return rc;
 }
 
