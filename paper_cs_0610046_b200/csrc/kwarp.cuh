@@ -82,6 +82,17 @@ struct PairLoader {  // the max-min filter: both chains read the same staged buf
   }
 };
 
+template <typename T>
+struct TwoLoader {  // the max chain over A, the min chain over B
+  const unsigned char *A, *B;
+  static constexpr bool TWO = true;
+  template <int N>
+  __device__ __forceinline__ void load(int pos, T (&ya)[N], T (&yb)[N]) const {
+    lds_swz<T, N>(A, pos, ya);
+    lds_swz<T, N>(B, pos, yb);
+  }
+};
+
 template <typename T, int E, int G, class Ld>
 __device__ __forceinline__ void warp_window_med(const Ld &ld, int pos0, const WarpGeom &g, const WarpAgg<T> &agg,
                                                 int lane, T (&ox)[E], T (&on)[E]) {

@@ -142,6 +142,9 @@ __device__ __forceinline__ void morph_window(const unsigned char *X, int pos0, c
     warp_window_med<T, E, G>(PairLoader<T>{X}, pos0, g, agg, lane, ox, on);
 }
 
+#ifndef MM_MORPH_P2PAIR
+#define MM_MORPH_P2PAIR 1  // pass 2 as one paired call (7% faster than two single chains)
+#endif
 #ifndef MM_MORPH_MINB
 #define MM_MORPH_MINB 1
 #endif
@@ -234,8 +237,12 @@ __global__ void __launch_bounds__(32 * kMorphWarps, MM_MORPH_MINB) k_morph_fused
         warp_window_small1<T, E, true>(EB, OFF - (w - 1), w, lane, op);
         warp_window_small1<T, E, false>(DB, OFF - (w - 1), w, lane, cl);
       } else {
+#if MM_MORPH_P2PAIR
+        warp_window_med<T, E, G>(TwoLoader<T>{EB, DB}, OFF - (w - 1), a.g, agg, lane, op, cl);
+#else
         warp_window_med1<T, E, G, true>(EB, OFF - (w - 1), a.g, agg, lane, op);
         warp_window_med1<T, E, G, false>(DB, OFF - (w - 1), a.g, agg, lane, cl);
+#endif
       }
       const int64_t i0 = j0 + lane * E;
       const int64_t left = a.n - i0;
