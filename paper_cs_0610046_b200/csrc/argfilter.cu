@@ -357,38 +357,16 @@ __global__ void __launch_bounds__(32 * kArgWarps) k_arg_fused(ArgArgs a) {
 template <typename S, int G>
 int launch_arg_g(ArgArgs a, cudaStream_t s) {
   using Geo = ArgGeo<S>;
-  int best_ns = 0, best_nw = 0;
-  int64_t best = -1;
-  for (int nwb = kArgWarps; nwb >= 1; nwb /= 2) {
-    for (int ns = 2; ns <= 4; ++ns) {
-      const size_t bytes = Geo::cta_bytes(a.w, ns, nwb);
-      if (bytes > 227 * 1024) continue;
-      cudaError_t e = cudaFuncSetAttribute(k_arg_fused<S, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-      if (e != cudaSuccess) return note_cuda(e);
-      int per = 0;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_arg_fused<S, G>, 32 * nwb, bytes);
-      if (e != cudaSuccess) return note_cuda(e);
-      const int64_t score = ((int64_t)per * nwb) * 8 + (ns - 1);  // resident warps first
-      if (per > 0 && score > best) {
-        best = score;
-        best_ns = ns;
-        best_nw = nwb;
-      }
-    }
-  }
-  if (best < 0) return kErrUnsupported;
-  a.nstages = best_ns;
+  WarpLaunch L;  // resident warps first
+  int rc = warp_launch_choice(reinterpret_cast<const void *>(k_arg_fused<S, G>), a.w, kArgWarps, 1,
+                              [](int w, int ns, int nw) { return Geo::cta_bytes(w, ns, nw); }, 1, &L);
+  if (rc) return rc;
+  a.nstages = L.ns;
   a.stage_bytes = Geo::stage_bytes(a.w);
-  a.warp_bytes = Geo::warp_bytes(a.w, best_ns);
-  const size_t smem = Geo::cta_bytes(a.w, best_ns, best_nw);
-  cudaError_t e = cudaFuncSetAttribute(k_arg_fused<S, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return note_cuda(e);
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_arg_fused<S, G>, 32 * best_nw, smem);
-  if (e != cudaSuccess) return note_cuda(e);
-  const int64_t want = (a.nseg + best_nw - 1) / best_nw;
-  const int64_t cap = (int64_t)sm_count() * per_sm;
-  k_arg_fused<S, G><<<(int)(want < cap ? want : cap), 32 * best_nw, smem, s>>>(a);
+  a.warp_bytes = Geo::warp_bytes(a.w, L.ns);
+  const int64_t want = (a.nseg + L.nw - 1) / L.nw;
+  const int64_t cap = (int64_t)sm_count() * L.per_sm;
+  k_arg_fused<S, G><<<(int)(want < cap ? want : cap), 32 * L.nw, L.smem, s>>>(a);
   return note_cuda(cudaGetLastError());
 }
 

@@ -35,6 +35,20 @@ template <typename T>
 int launch_argfilter(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w, void *out_max,
                      void *out_min, int64_t *arg_max, int64_t *arg_min, int64_t out_ld, void *ws,
                      size_t ws_bytes, cudaStream_t s);
+// Launch shape of a warp-autonomous kernel (stream.cu, morph.cu, argfilter.cu):
+// warps per CTA (nw in {max_nw, max_nw/2, ..., min_nw}) and staging depth ns
+// (2..4), from the occupancy API, cached per (kernel, w) -- the queries cost
+// microseconds, a push tens.  The kernel's dynamic shared memory limit only
+// grows, under a lock, so concurrent host threads never shrink it under a
+// launch in flight (maxmin_abi.cu).
+struct WarpLaunch {
+  int ns, nw, per_sm;
+  size_t smem;
+};
+using WarpBytesFn = size_t (*)(int w, int ns, int nw);
+int warp_launch_choice(const void *kern, int w, int max_nw, int min_nw, WarpBytesFn bytes, int prefer_warps,
+                       WarpLaunch *out);
+
 // online multi-stream filter (stream.cu)
 struct StreamLayout {
   int fused;          // one fused kernel per push (ping-pong history rows) or the composition

@@ -10,6 +10,9 @@
 #include "../../include/maxmin.h"
 #include "launch.cuh"
 
+#include <map>
+#include <mutex>
+
 namespace mm {
 
 static thread_local int g_last_cuda_error = 0;
@@ -113,6 +116,57 @@ MM_DECLARE_INST(double)
     case MAXMIN_F64: { using T = double; CALL; }   \
     default: return MAXMIN_ERR_DTYPE;             \
   }
+
+namespace mm {
+int warp_launch_choice(const void *kern, int w, int max_nw, int min_nw, WarpBytesFn bytes, int prefer_warps,
+                       WarpLaunch *out) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, WarpLaunch> cache;
+  static std::map<const void *, size_t> attr;  // dynamic smem limit set so far, per kernel
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return note_cuda(e);
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_pair(kern, w * 64 + dev);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return kOK;
+  }
+  auto raise_limit = [&](size_t b) -> int {
+    size_t &cur = attr[kern];
+    if (b <= cur) return kOK;
+    cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+    if (r != cudaSuccess) return note_cuda(r);
+    cur = b;
+    return kOK;
+  };
+  WarpLaunch best{0, 0, 0, 0};
+  int64_t best_score = -1;
+  for (int nw = max_nw; nw >= min_nw; nw /= 2) {
+    for (int ns = 2; ns <= 4; ++ns) {
+      const size_t b = bytes(w, ns, nw);
+      if (b > 227 * 1024) continue;
+      int rc = raise_limit(b);
+      if (rc) return rc;
+      int per = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 32 * nw, b);
+      if (e != cudaSuccess) return note_cuda(e);
+      if (per < 1) continue;
+      const int64_t warps = (int64_t)per * nw;
+      const int64_t score = prefer_warps ? warps * 8 + (ns - 1) : warps * (ns - 1);
+      if (score > best_score) {
+        best_score = score;
+        best = WarpLaunch{ns, nw, per, b};
+      }
+    }
+  }
+  if (best_score < 0) return kErrUnsupported;
+  cache[key] = best;
+  *out = best;
+  return kOK;
+}
+}  // namespace mm
 
 namespace {
 

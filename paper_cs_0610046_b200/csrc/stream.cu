@@ -303,47 +303,22 @@ StreamLayout stream_layout(int64_t streams, int64_t w, int64_t max_chunk) {
 template <typename T, int E, int G>
 int launch_fused_g(StreamArgs a, cudaStream_t s) {
   using Geo = StreamGeo<T, E>;
-  // staging depth: the most segments in flight per SM (3 CTAs fit the registers)
-  // staging depth: the most segments in flight per SM (occupancy from registers and smem)
-  int best = 2;
-  {
-    int64_t best_fly = -1;
-    for (int ns = 2; ns <= 4; ++ns) {
-      const size_t sm_bytes = Geo::cta_bytes(a.w, ns);
-      if (sm_bytes > 227 * 1024) continue;
-      cudaError_t e = cudaFuncSetAttribute(k_stream_fused<T, E, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes);
-      if (e != cudaSuccess) return note_cuda(e);
-      int per = 0;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_stream_fused<T, E, G>, 32 * kStreamWarps, sm_bytes);
-      if (e != cudaSuccess) return note_cuda(e);
-      const int64_t fly = (int64_t)per * kStreamWarps * (ns - 1);
-      if (fly > best_fly) {
-        best_fly = fly;
-        best = ns;
-      }
-    }
-  }
-  a.nstages = best;
-  a.stage_bytes = Geo::stage_bytes(a.w);
-  a.warp_bytes = Geo::warp_bytes(a.w, best);
   a.segs_per_row = (a.c + Geo::SEG - 1) / Geo::SEG;
   a.nseg = a.streams * a.segs_per_row;
   if (a.nseg > 0x7fffffffLL) return kErrUnsupported;
   a.g = make_warp_geom<E>(a.w, G);
   if (a.g.V + 32 / G > WarpAgg<T>::AGG) return kErrUnsupported;
-  const size_t smem = Geo::cta_bytes(a.w, best);
-  {
-    cudaError_t e = cudaFuncSetAttribute(k_stream_fused<T, E, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return note_cuda(e);
-  }
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stream_fused<T, E, G>, 32 * kStreamWarps, smem);
-  if (e != cudaSuccess) return note_cuda(e);
-  if (per_sm < 1) return kErrUnsupported;
+  // staging depth: the most segments in flight per SM
+  WarpLaunch L;
+  int rc = warp_launch_choice(reinterpret_cast<const void *>(k_stream_fused<T, E, G>), a.w, kStreamWarps, kStreamWarps,
+                              [](int w, int ns, int) { return Geo::cta_bytes(w, ns); }, 0, &L);
+  if (rc) return rc;
+  a.nstages = L.ns;
+  a.stage_bytes = Geo::stage_bytes(a.w);
+  a.warp_bytes = Geo::warp_bytes(a.w, L.ns);
   const int64_t want = (a.nseg + kStreamWarps - 1) / kStreamWarps;
-  const int64_t cap = (int64_t)sm_count() * per_sm;
-  const int grid = (int)(want < cap ? want : cap);
-  k_stream_fused<T, E, G><<<grid, 32 * kStreamWarps, smem, s>>>(a);
+  const int64_t cap = (int64_t)sm_count() * L.per_sm;
+  k_stream_fused<T, E, G><<<(int)(want < cap ? want : cap), 32 * kStreamWarps, L.smem, s>>>(a);
   return note_cuda(cudaGetLastError());
 }
 
