@@ -41,6 +41,11 @@ int launch_argfilter(const void *in, int64_t batch, int64_t n, int64_t in_ld, in
 // microseconds, a push tens.  The kernel's dynamic shared memory limit only
 // grows, under a lock, so concurrent host threads never shrink it under a
 // launch in flight (maxmin_abi.cu).
+// Raise a kernel's dynamic shared memory limit to at least `bytes` on the
+// current device; the limit only grows, under a lock (concurrent host threads
+// never lower it under another thread's launch).  maxmin_abi.cu.
+int raise_smem_limit(const void *kern, size_t bytes);
+
 struct WarpLaunch {
   int ns, nw, per_sm;
   size_t smem;
@@ -145,11 +150,8 @@ static int occupancy_grid(K kernel, size_t smem, int64_t ntiles, int &grid) {
 
 template <typename K>
 static int set_smem(K kernel, size_t bytes, size_t &done) {
-  if (done >= bytes) return kOK;
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e != cudaSuccess) return note_cuda(e);
-  done = bytes;
-  return kOK;
+  (void)done;  // the limit is tracked per (kernel, device) under a lock: raise_smem_limit
+  return raise_smem_limit(reinterpret_cast<const void *>(kernel), bytes);
 }
 
 template <typename T, int W, class Epi = StoreEpi>
@@ -340,9 +342,7 @@ static int launch_warp(const Rows &p, void *ws, size_t ws_bytes, cudaStream_t s)
       }
     }
     constexpr size_t smem = Geo::BYTES;
-    rc = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess
-             ? kOK
-             : note_cuda(cudaGetLastError());
+    rc = raise_smem_limit(reinterpret_cast<const void *>(kern), smem);
     if (rc) return rc;
     int grid = 0;
     rc = occupancy_grid(kern, smem, (g.total + NWARP - 1) / NWARP, grid);

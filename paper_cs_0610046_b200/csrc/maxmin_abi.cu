@@ -118,29 +118,41 @@ MM_DECLARE_INST(double)
   }
 
 namespace mm {
-int warp_launch_choice(const void *kern, int w, int max_nw, int min_nw, WarpBytesFn bytes, int prefer_warps,
-                       WarpLaunch *out) {
-  static std::mutex mu;
-  static std::map<std::pair<const void *, int>, WarpLaunch> cache;
-  static std::map<const void *, size_t> attr;  // dynamic smem limit set so far, per kernel
+static std::mutex g_launch_mu;  // guards the two maps below
+
+// dynamic smem limit set so far, per (kernel, device); callers hold g_launch_mu
+static int raise_smem_limit_locked(const void *kern, int dev, size_t b) {
+  static std::map<std::pair<const void *, int>, size_t> attr;
+  size_t &cur = attr[std::make_pair(kern, dev)];
+  if (b <= cur) return kOK;
+  cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+  if (r != cudaSuccess) return note_cuda(r);
+  cur = b;
+  return kOK;
+}
+
+int raise_smem_limit(const void *kern, size_t bytes) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return note_cuda(e);
-  std::lock_guard<std::mutex> lock(mu);
-  const auto key = std::make_pair(kern, w * 64 + dev);
+  std::lock_guard<std::mutex> lock(g_launch_mu);
+  return raise_smem_limit_locked(kern, dev, bytes);
+}
+
+int warp_launch_choice(const void *kern, int w, int max_nw, int min_nw, WarpBytesFn bytes, int prefer_warps,
+                       WarpLaunch *out) {
+  static std::map<std::pair<const void *, int64_t>, WarpLaunch> cache;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return note_cuda(e);
+  std::lock_guard<std::mutex> lock(g_launch_mu);
+  const auto key = std::make_pair(kern, (int64_t)w * 1024 + dev);
   auto it = cache.find(key);
   if (it != cache.end()) {
     *out = it->second;
     return kOK;
   }
-  auto raise_limit = [&](size_t b) -> int {
-    size_t &cur = attr[kern];
-    if (b <= cur) return kOK;
-    cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
-    if (r != cudaSuccess) return note_cuda(r);
-    cur = b;
-    return kOK;
-  };
+  auto raise_limit = [&](size_t b) -> int { return raise_smem_limit_locked(kern, dev, b); };
   WarpLaunch best{0, 0, 0, 0};
   int64_t best_score = -1;
   for (int nw = max_nw; nw >= min_nw; nw /= 2) {
