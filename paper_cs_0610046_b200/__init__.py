@@ -10,6 +10,7 @@ is no CPU fallback -- a missing library raises.
 from __future__ import annotations
 
 import ctypes
+import functools
 
 import torch
 
@@ -42,19 +43,34 @@ def version() -> str:
     return _lib.lib().maxmin_version().decode()
 
 
-def _stream_ptr(stream) -> ctypes.c_void_p:
-    s = torch.cuda.current_stream() if stream is None else stream
-    return ctypes.c_void_p(s.cuda_stream)
+try:  # the raw handle of the current stream without building a Stream object (~0.3 us)
+    _raw_stream = torch._C._cuda_getCurrentRawStream
+except AttributeError:  # pragma: no cover
+    _raw_stream = None
+
+
+def _stream_ptr(stream, device=None) -> ctypes.c_void_p:
+    if stream is None:
+        if _raw_stream is not None:
+            idx = torch.cuda.current_device() if device is None else device.index
+            return ctypes.c_void_p(_raw_stream(idx))
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
 
 
 def _ptr(t) -> ctypes.c_void_p:
     return ctypes.c_void_p(0 if t is None else t.data_ptr())
 
 
-def maxmin_workspace_bytes(dtype, batch: int, n: int, w: int) -> int:
+@functools.lru_cache(maxsize=256)
+def _workspace_bytes(code: int, batch: int, n: int, w: int) -> int:
     out = ctypes.c_size_t(0)
-    _lib.check(_lib.lib().maxmin_workspace_bytes(dtype_code(dtype), batch, n, w, ctypes.byref(out)))
+    _lib.check(_lib.lib().maxmin_workspace_bytes(code, batch, n, w, ctypes.byref(out)))
     return int(out.value)
+
+
+def maxmin_workspace_bytes(dtype, batch: int, n: int, w: int) -> int:
+    return _workspace_bytes(dtype_code(dtype), batch, n, w)
 
 
 def _workspace(dtype, batch, n, w, device, workspace):
@@ -79,7 +95,7 @@ def maxmin_filter_1d(x: torch.Tensor, w: int, out_max=None, out_min=None, *, wan
         out_min = torch.empty(m, dtype=x.dtype, device=x.device)
     ws, wsb = _workspace(x.dtype, 1, n, w, x.device, workspace) if 1 <= w <= n else (None, 0)
     _lib.check(_lib.lib().maxmin_filter_1d(dtype_code(x.dtype), _ptr(x), n, w, _ptr(out_max),
-                                           _ptr(out_min), _ptr(ws), wsb, _stream_ptr(stream)))
+                                           _ptr(out_min), _ptr(ws), wsb, _stream_ptr(stream, x.device)))
     return out_max, out_min
 
 
@@ -102,7 +118,7 @@ def maxmin_filter_batched(x: torch.Tensor, w: int, n: int | None = None, out_max
     ws, wsb = _workspace(x.dtype, batch, n, w, x.device, workspace) if 1 <= w <= n else (None, 0)
     _lib.check(_lib.lib().maxmin_filter_batched(dtype_code(x.dtype), _ptr(x), batch, n, x.stride(0), w,
                                                 _ptr(out_max), _ptr(out_min), out_ld, _ptr(ws), wsb,
-                                                _stream_ptr(stream)))
+                                                _stream_ptr(stream, x.device)))
     return out_max, out_min
 
 

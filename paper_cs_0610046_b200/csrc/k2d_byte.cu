@@ -16,8 +16,8 @@ static int launch_byte(const k2b::Args &a, const CUtensorMap &map, cudaStream_t 
   int rc = set_smem(kern, smem, attr);
   if (rc) return rc;
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, k2b::NTB, smem);
-  if (e != cudaSuccess) return note_cuda(e);
+  rc = blocks_per_sm(reinterpret_cast<const void *>(kern), k2b::NTB, smem, &per_sm);
+  if (rc) return rc;
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)per_sm * sm_count();
   if (grid > a.ntiles) grid = a.ntiles;

@@ -45,6 +45,9 @@ int launch_argfilter(const void *in, int64_t batch, int64_t n, int64_t in_ld, in
 // current device; the limit only grows, under a lock (concurrent host threads
 // never lower it under another thread's launch).  maxmin_abi.cu.
 int raise_smem_limit(const void *kern, size_t bytes);
+// Resident CTAs per SM of a kernel (cudaOccupancyMaxActiveBlocksPerMultiprocessor),
+// cached per (kernel, device, threads, smem): the query costs microseconds.
+int blocks_per_sm(const void *kern, int threads, size_t smem, int *per_sm);
 
 struct WarpLaunch {
   int ns, nw, per_sm;
@@ -140,8 +143,8 @@ size_t workspace_1d(int64_t batch, int64_t n, int64_t w) {
 template <typename K>
 static int occupancy_grid(K kernel, size_t smem, int64_t ntiles, int &grid) {
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, NT, smem);
-  if (e != cudaSuccess) return note_cuda(e);
+  int rc = blocks_per_sm(reinterpret_cast<const void *>(kernel), NT, smem, &per_sm);
+  if (rc) return rc;
   if (per_sm < 1) per_sm = 1;
   int64_t cap = (int64_t)per_sm * sm_count();
   grid = (int)(ntiles < cap ? ntiles : cap);

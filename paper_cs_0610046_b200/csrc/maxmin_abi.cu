@@ -12,6 +12,7 @@
 
 #include <map>
 #include <mutex>
+#include <tuple>
 
 namespace mm {
 
@@ -137,6 +138,24 @@ int raise_smem_limit(const void *kern, size_t bytes) {
   if (e != cudaSuccess) return note_cuda(e);
   std::lock_guard<std::mutex> lock(g_launch_mu);
   return raise_smem_limit_locked(kern, dev, bytes);
+}
+
+int blocks_per_sm(const void *kern, int threads, size_t smem, int *per_sm) {
+  static std::map<std::tuple<const void *, int, int, size_t>, int> cache;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return note_cuda(e);
+  std::lock_guard<std::mutex> lock(g_launch_mu);
+  const auto key = std::make_tuple(kern, dev, threads, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *per_sm = it->second;
+    return kOK;
+  }
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kern, threads, smem);
+  if (e != cudaSuccess) return note_cuda(e);
+  cache[key] = *per_sm;
+  return kOK;
 }
 
 int warp_launch_choice(const void *kern, int w, int max_nw, int min_nw, WarpBytesFn bytes, int prefer_warps,
