@@ -221,18 +221,6 @@ struct ArgArgs {
   int w, in_vec, out_vec, stage_bytes, warp_bytes, nstages;
 };
 
-__device__ __forceinline__ void acp_async16(void *smem, const void *g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
-}
-__device__ __forceinline__ void acp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void acp_async_wait_ring(int n) {
-  if (n >= 4)
-    asm volatile("cp.async.wait_group 3;" ::: "memory");
-  else if (n == 3)
-    asm volatile("cp.async.wait_group 2;" ::: "memory");
-  else
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-}
 
 template <typename S>
 __device__ __forceinline__ void arg_stage(const ArgArgs &a, unsigned char *X, int64_t row, int64_t j0, int lane) {
@@ -245,7 +233,7 @@ __device__ __forceinline__ void arg_stage(const ArgArgs &a, unsigned char *X, in
     const int64_t v = j0 + (int64_t)q * VEC;
     unsigned char *dst = X + swz(q);
     if (a.in_vec && v + VEC <= a.n) {
-      acp_async16(dst, src + v);
+      cp_async16(dst, src + v);
     } else {
       S t[VEC];
 #pragma unroll
@@ -283,7 +271,7 @@ __global__ void __launch_bounds__(32 * kArgWarps) k_arg_fused(ArgArgs a) {
       seg_pos(sg, row, j0);
       arg_stage<S>(a, stg(k), row, j0, lane);
     }
-    acp_async_commit();
+    cp_async_commit();
   }
   int slot = 0;
   for (int64_t sg = gw; sg < a.nseg; sg += nw) {
@@ -295,8 +283,8 @@ __global__ void __launch_bounds__(32 * kArgWarps) k_arg_fused(ArgArgs a) {
         arg_stage<S>(a, stg(slot + ns - 1 < ns ? slot + ns - 1 : slot - 1), row, j0, lane);
       }
     }
-    acp_async_commit();
-    acp_async_wait_ring(ns);
+    cp_async_commit();
+    cp_async_wait_ring(ns);
     __syncwarp();
     const unsigned char *X = stg(slot);
     slot = slot + 1 < ns ? slot + 1 : 0;

@@ -25,6 +25,22 @@
 
 namespace mm {
 
+// cp.async staging for the warp-autonomous kernels: 16-B copies global ->
+// shared, committed per segment; a ring of n stages keeps n-1 segments in flight.
+__device__ __forceinline__ void cp_async16(void *smem, const void *g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// wait until at most n-1 copy groups are pending (n = 2..4, warp-uniform)
+__device__ __forceinline__ void cp_async_wait_ring(int n) {
+  if (n >= 4)
+    asm volatile("cp.async.wait_group 3;" ::: "memory");
+  else if (n == 3)
+    asm volatile("cp.async.wait_group 2;" ::: "memory");
+  else
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+}
+
 // Gap geometry of block B = E*G for window w (E <= w-1): D = w-1-B = q'B + r'.
 struct WarpGeom {
   int w;

@@ -82,18 +82,6 @@ struct MorphArgs {
   int stage_bytes, ebuf_bytes, warp_bytes, nstages;
 };
 
-__device__ __forceinline__ void mcp_async16(void *smem, const void *g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
-}
-__device__ __forceinline__ void mcp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void mcp_async_wait_ring(int n) {
-  if (n >= 4)
-    asm volatile("cp.async.wait_group 3;" ::: "memory");
-  else if (n == 3)
-    asm volatile("cp.async.wait_group 2;" ::: "memory");
-  else
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-}
 
 // stage f[j0, j0 + SEG + w - 1) of `row` (j0 is a multiple of SEG: 16-B aligned)
 template <typename T>
@@ -108,7 +96,7 @@ __device__ __forceinline__ void morph_stage(const MorphArgs &a, unsigned char *X
     const int64_t v = j0 + (int64_t)q * VEC;
     unsigned char *dst = X + swz(q);
     if (a.in_vec && v + VEC <= a.n) {
-      mcp_async16(dst, src + v);
+      cp_async16(dst, src + v);
     } else {
       T t[VEC];
 #pragma unroll
@@ -189,7 +177,7 @@ __global__ void __launch_bounds__(32 * kMorphWarps, MM_MORPH_MINB) k_morph_fused
       seg_pos(sg, row, j0);
       morph_stage<T>(a, stg(k), row, j0, lane);
     }
-    mcp_async_commit();
+    cp_async_commit();
   }
   int slot = 0;
   for (int64_t sg = s_first; sg < s_end; ++sg) {
@@ -201,8 +189,8 @@ __global__ void __launch_bounds__(32 * kMorphWarps, MM_MORPH_MINB) k_morph_fused
         morph_stage<T>(a, stg(slot + ns - 1 < ns ? slot + ns - 1 : slot - 1), row, j0, lane);
       }
     }
-    mcp_async_commit();
-    mcp_async_wait_ring(ns);
+    cp_async_commit();
+    cp_async_wait_ring(ns);
     __syncwarp();
     const unsigned char *X = stg(slot);
     slot = slot + 1 < ns ? slot + 1 : 0;

@@ -131,19 +131,6 @@ struct StreamArgs {
   int nstages;         // staging ring per warp: 2..4 (nstages-1 segments in flight)
 };
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-// wait until at most n-1 copy groups are pending (n = 2..4, warp-uniform)
-__device__ __forceinline__ void cp_async_wait_ring(int n) {
-  if (n >= 4)
-    asm volatile("cp.async.wait_group 3;" ::: "memory");
-  else if (n == 3)
-    asm volatile("cp.async.wait_group 2;" ::: "memory");
-  else
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-}
 
 // Stage V'[j0, j0 + len) of `row` into the swizzled buffer X (logical index
 // i = V' index - j0).  j0 and hld are multiples of VEC, so every 16-B unit
