@@ -622,3 +622,42 @@ def test_morph_2d(cuda_device, wr, wc, dtype):
     eo, ec = oracle.morph_2d(a, wr, wc)
     assert_same(op, eo, "open 2d")
     assert_same(cl, ec, "close 2d")
+
+
+# ------------------------------------------------ NEXT rows: API corner cases
+def test_stream_single_output_and_reuse(cuda_device):
+    """One output array per push (max only / min only), preallocated outputs reused."""
+    rows = synth.c3(rows=33, length=600)
+    w, c = 40, 150
+    x = torch.from_numpy(rows).to(dev())
+    exp = oracle.stream_pushes(rows, w, [c] * 4)
+    sx = mm.MaxMinStream(torch.float32, 33, w, c, device=dev())
+    sn = mm.MaxMinStream(torch.float32, 33, w, c, device=dev())
+    ox = torch.empty(33, 152, dtype=torch.float32, device=dev())[:, :c]
+    on = torch.empty(33, 152, dtype=torch.float32, device=dev())[:, :c]
+    for p in range(4):
+        ch = x[:, p * c:(p + 1) * c].contiguous()
+        mx, none1, fv = sx.push(ch, out_max=ox, want_min=False)
+        none2, mn, fv2 = sn.push(ch, out_min=on, want_max=False)
+        torch.cuda.synchronize()
+        assert none1 is None and none2 is None and fv == fv2
+        assert_same(mx[:, fv:], exp[p][0], f"max push {p}")
+        assert_same(mn[:, fv:], exp[p][1], f"min push {p}")
+
+
+def test_morph_2d_strided_input_single_output(cuda_device):
+    a = synth.random_values(np.float32, 3 * 50 * 70, seed=12).reshape(3, 50, 70)
+    x = torch.from_numpy(a).to(dev())
+    op, cl = mm.maxmin_morph_2d(x, 5, 3, cols=61, want_close=False)  # the first 61 columns of each row
+    torch.cuda.synchronize()
+    assert cl is None
+    eo, _ = oracle.morph_2d(np.ascontiguousarray(a[:, :, :61]), 5, 3)
+    assert_same(op, eo, "open 2d strided")
+
+
+def test_keogh_rows_shorter_than_pitch(cuda_device):
+    c = synth.c3(rows=20, length=1000, ld=1004)
+    q = synth.c3(rows=1, row0=99, length=1000)[0]
+    lb = mm.maxmin_lb_keogh_batched(torch.from_numpy(c).to(dev()), torch.from_numpy(q).to(dev()), 30, n=1000)
+    ref = oracle.keogh(np.ascontiguousarray(c[:, :1000]), q, 30)
+    _keogh_close(lb, ref)
