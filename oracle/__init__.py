@@ -23,6 +23,7 @@ cites the PAPER.md passage it follows:
 ``keogh``              N3 LB_Keogh (clipped envelope, R18)
 ``Stream``             N2 one stream's wedge, zero-latency pushes (R19)
 ``morph`` / ``morph_2d`` N4 opening and closing (definition or composition, R20)
+``brute_3d`` / ``separable_3d`` N4 N-D separable filter: 3-D boxes (definition / axis by axis)
 =====================  ====================================================
 
 Parity pins live in ``tests/test_oracle_*.py``; none of the functions is
@@ -332,3 +333,24 @@ def morph_2d(a, w_row: int, w_col: int, brute: bool = False):
         _ptr(a), ctypes.c_int64(batch), ctypes.c_int64(rows), ctypes.c_int64(cols), ctypes.c_int64(w_row),
         ctypes.c_int64(w_col), _ptr(op), _ptr(cl)))
     return (op[0], cl[0]) if squeeze else (op, cl)
+
+
+def _run_3d(name: str, a, w_x: int, w_y: int, w_z: int):
+    a = np.ascontiguousarray(a)
+    depth, rows, cols = a.shape
+    D, R, C = depth - w_z + 1, rows - w_y + 1, cols - w_x + 1
+    mx = np.empty((max(D, 0), max(R, 0), max(C, 0)), a.dtype)
+    mn = np.empty_like(mx)
+    _check(_fn(name, a.dtype)(_ptr(a), ctypes.c_int64(depth), ctypes.c_int64(rows), ctypes.c_int64(cols),
+                              ctypes.c_int64(w_x), ctypes.c_int64(w_y), ctypes.c_int64(w_z), _ptr(mx), _ptr(mn)))
+    return mx, mn
+
+
+def brute_3d(a, w_x: int, w_y: int, w_z: int):
+    """3-D max/min over w_z x w_y x w_x boxes, valid region (the definition)."""
+    return _run_3d("brute_3d", a, w_x, w_y, w_z)
+
+
+def separable_3d(a, w_x: int, w_y: int, w_z: int):
+    """The 1-D filter along columns, rows, then depth (PAPER.md:61-63 extended)."""
+    return _run_3d("separable_3d", a, w_x, w_y, w_z)

@@ -101,6 +101,12 @@ int oracle_stream_stats(const oracle_stream *s, oracle_stats *st);
   int oracle_morph_2d_##S(const T *a, int64_t batch, int64_t rows,              \
                           int64_t cols, int64_t w_row, int64_t w_col,           \
                           T *open, T *close);                                   \
+  int oracle_brute_3d_##S(const T *a, int64_t depth, int64_t rows,             \
+                          int64_t cols, int64_t w_x, int64_t w_y, int64_t w_z,  \
+                          T *out_max, T *out_min);                              \
+  int oracle_separable_3d_##S(const T *a, int64_t depth, int64_t rows,         \
+                              int64_t cols, int64_t w_x, int64_t w_y,           \
+                              int64_t w_z, T *out_max, T *out_min);             \
   int oracle_stream_new_##S(int64_t w, oracle_stream **out);                    \
   int oracle_stream_push_##S(oracle_stream *s, const T *x, int64_t c,           \
                              T *out_max, T *out_min, int64_t *emitted);

@@ -552,3 +552,25 @@ def test_morph_2d_brute_and_scipy():
     r1o, r1c = oracle.morph(a[3], 5)  # one row, w_col = 1: the 1-D operators
     o1, c1 = oracle.morph_2d(a[3:4], 5, 1)
     assert same(o1[0], r1o) and same(c1[0], r1c)
+
+
+# ---------------------------------------------------------- N4: 3-D filters
+def test_3d_brute_equals_separable():
+    rng = np.random.default_rng(5)
+    for (d, r, c, wx, wy, wz) in [(4, 5, 6, 2, 3, 2), (3, 3, 3, 3, 3, 3), (5, 4, 7, 1, 1, 5), (6, 2, 9, 4, 2, 1),
+                                  (7, 6, 5, 5, 6, 3)]:
+        for dt in (np.uint8, np.int32, np.float64):
+            a = rng.integers(0, 4, size=(d, r, c)).astype(dt)
+            bx, bn = oracle.brute_3d(a, wx, wy, wz)
+            sx, sn = oracle.separable_3d(a, wx, wy, wz)
+            assert same(bx, sx) and same(bn, sn), (d, r, c, wx, wy, wz, dt)
+
+
+def test_3d_vs_numpy_and_2d():
+    a = synth.random_values(np.dtype(np.float32), 9 * 20 * 23, seed=8).reshape(9, 20, 23)
+    v = swv(a, (3, 4, 5), axis=(0, 1, 2))  # windows of w_z=3, w_y=4, w_x=5
+    mx, mn = oracle.separable_3d(a, 5, 4, 3)
+    assert same(mx, v.max(axis=(-3, -2, -1))) and same(mn, v.min(axis=(-3, -2, -1)))
+    m2x, m2n = oracle.separable_2d(a, 5, 4)  # w_z = 1 is the 2-D filter of every slice
+    m3x, m3n = oracle.separable_3d(a, 5, 4, 1)
+    assert same(m2x, m3x) and same(m2n, m3n)
