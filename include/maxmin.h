@@ -265,6 +265,28 @@ int maxmin_morph_2d(int dt, const void *in, int64_t batch, int64_t rows, int64_t
                     void *workspace, size_t workspace_bytes, void *stream);
 
 /*
+ * The max-min filter over 3-D boxes ("N-D separable
+ * filters"; the paper's rows-then-columns application, with
+ * a depth axis): for a volume of `depth` slices of rows x cols (row pitch
+ * in_ld, slice pitch in_slice, elements),
+ *   out(k,i,j) = max / min over [k, k+w_z) x [i, i+w_y) x [j, j+w_x)
+ * for the valid region D' x R' x C' = (depth-w_z+1) x (rows-w_y+1) x
+ * (cols-w_x+1); outputs with row pitch out_ld and slice pitch out_slice
+ * (either output may be NULL).  Element alignment suffices.  Device
+ * workspace of maxmin_filter_3d_workspace_bytes (two scratch volumes of D'
+ * slices).  Runs as the 2-D kernel along depth (slices as rows, window
+ * 1 x w_z), then the 2-D filter (w_x, w_y) of every scratch slice.
+ * MAXMIN_ERR_UNSUPPORTED when the depth window exceeds the 2-D kernel's
+ * shared memory (about w_z > 140 for 4-byte types).
+ */
+int maxmin_filter_3d_workspace_bytes(int dt, int64_t depth, int64_t rows, int64_t cols,
+                                     int64_t in_ld, int64_t w_z, size_t *bytes);
+int maxmin_filter_3d(int dt, const void *in, int64_t depth, int64_t rows, int64_t cols,
+                     int64_t in_ld, int64_t in_slice, int64_t w_x, int64_t w_y, int64_t w_z,
+                     void *out_max, void *out_min, int64_t out_ld, int64_t out_slice,
+                     void *workspace, size_t workspace_bytes, void *stream);
+
+/*
  * End-to-end 1-D call on HOST buffers (in, out_max, out_min are host
  * pointers; page-locked memory gives full PCIe bandwidth).  The input is
  * streamed to the device in chunks (with a (w-1)-element overlap), filtered

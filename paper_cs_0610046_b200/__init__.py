@@ -22,7 +22,7 @@ __all__ = [
     "maxmin_filter_batched", "maxmin_filter_2d", "maxmin_filter_1d_host",
     "maxmin_host_workspace_bytes", "maxmin_argfilter_workspace_bytes", "maxmin_argfilter_batched",
     "maxmin_argfilter_1d", "maxmin_lb_keogh_batched", "maxmin_stream_state_bytes", "MaxMinStream", "maxmin_morph_batched",
-    "maxmin_morph_1d", "maxmin_morph_2d", "version",
+    "maxmin_morph_1d", "maxmin_morph_2d", "maxmin_filter_3d", "version",
 ]
 
 _CODES = {
@@ -332,6 +332,32 @@ def maxmin_morph_2d(x: torch.Tensor, w_row: int, w_col: int, cols: int | None = 
         out_open = out_open[0] if out_open is not None and out_open.dim() == 3 else out_open
         out_close = out_close[0] if out_close is not None and out_close.dim() == 3 else out_close
     return out_open, out_close
+
+
+def maxmin_filter_3d(x: torch.Tensor, w_x: int, w_y: int, w_z: int, cols: int | None = None, out_max=None,
+                     out_min=None, *, want_max=True, want_min=True, workspace=None, stream=None):
+    """Max and min over w_z x w_y x w_x boxes of a [depth, rows, ld] CUDA tensor (first `cols`
+    columns); outputs [depth-w_z+1, rows-w_y+1, cols-w_x+1] (valid region)."""
+    if x.dim() != 3 or not x.is_cuda or x.stride(2) != 1:
+        raise ValueError("maxmin_filter_3d: x must be a row-major [depth, rows, ld] CUDA tensor")
+    depth, rows, ld = x.shape
+    cols = ld if cols is None else cols
+    D, R, C = depth - w_z + 1, rows - w_y + 1, cols - w_x + 1
+    if want_max and out_max is None and min(D, R, C) > 0:
+        out_max = torch.empty(D, R, C, dtype=x.dtype, device=x.device)
+    if want_min and out_min is None and min(D, R, C) > 0:
+        out_min = torch.empty(D, R, C, dtype=x.dtype, device=x.device)
+    o = out_max if out_max is not None else out_min
+    need = ctypes.c_size_t(0)
+    _lib.check(_lib.lib().maxmin_filter_3d_workspace_bytes(dtype_code(x.dtype), depth, rows, cols, x.stride(1), w_z,
+                                                           ctypes.byref(need)))
+    if workspace is None:
+        workspace = torch.empty(max(need.value, 16), dtype=torch.uint8, device=x.device)
+    _lib.check(_lib.lib().maxmin_filter_3d(
+        dtype_code(x.dtype), _ptr(x), depth, rows, cols, x.stride(1), x.stride(0), w_x, w_y, w_z, _ptr(out_max),
+        _ptr(out_min), o.stride(1) if o is not None else C, o.stride(0) if o is not None else R * C, _ptr(workspace),
+        workspace.numel(), _stream_ptr(stream)))
+    return out_max, out_min
 
 
 def maxmin_host_workspace_bytes(dtype, n: int, w: int, chunk: int = 0) -> int:

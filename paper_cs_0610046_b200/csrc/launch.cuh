@@ -70,6 +70,13 @@ StreamLayout stream_layout(int64_t streams, int64_t w, int64_t max_chunk);
 template <typename T>
 int launch_stream_push(void *state, const StreamLayout &L, int64_t streams, int64_t w, int phase, const T *chunk,
                        int64_t c, int64_t chunk_ld, T *out_max, T *out_min, int64_t out_ld, cudaStream_t s);
+// 3-D boxes (filter3d.cu)
+template <typename T>
+size_t filter3d_workspace(int64_t depth, int64_t rows, int64_t cols, int64_t in_ld, int64_t w_z);
+template <typename T>
+int launch_3d(const void *in, int64_t depth, int64_t rows, int64_t cols, int64_t in_ld, int64_t in_slice,
+              int64_t w_x, int64_t w_y, int64_t w_z, void *out_max, void *out_min, int64_t out_ld, int64_t out_slice,
+              void *ws, cudaStream_t s);
 // grayscale opening / closing (morph.cu)
 template <typename T>
 int launch_morph(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_t w, void *out_open,

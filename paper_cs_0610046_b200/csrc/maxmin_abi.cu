@@ -645,6 +645,57 @@ int maxmin_morph_2d(int dt, const void *in, int64_t batch, int64_t rows, int64_t
                                                 out_close, out_ld, out_bstride, workspace, s))
 }
 
+// ------------------------------------------------------------ N4: 3-D boxes
+int maxmin_filter_3d_workspace_bytes(int dt, int64_t depth, int64_t rows, int64_t cols, int64_t in_ld, int64_t w_z,
+                                     size_t *bytes) {
+  if (!bytes) return MAXMIN_ERR_NULL;
+  *bytes = 0;
+  const size_t sz = maxmin_dtype_size(dt);
+  if (!sz) return MAXMIN_ERR_DTYPE;
+  if (w_z < 1) return MAXMIN_ERR_WINDOW;
+  if (depth < 1 || rows < 1 || cols < 1 || in_ld < cols) return MAXMIN_ERR_SHAPE;
+  if (w_z > depth) return MAXMIN_ERR_WINDOW_TOO_LARGE;
+  size_t t;
+  if (!extent(depth, rows * in_ld + 16, rows * in_ld + 16, sz, &t)) return MAXMIN_ERR_SHAPE;
+  MM_DISPATCH(dt, { *bytes = mm::filter3d_workspace<T>(depth, rows, cols, in_ld, w_z); return MAXMIN_OK; })
+}
+
+int maxmin_filter_3d(int dt, const void *in, int64_t depth, int64_t rows, int64_t cols, int64_t in_ld,
+                     int64_t in_slice, int64_t w_x, int64_t w_y, int64_t w_z, void *out_max, void *out_min,
+                     int64_t out_ld, int64_t out_slice, void *workspace, size_t workspace_bytes, void *stream) {
+  const size_t sz = maxmin_dtype_size(dt);
+  if (!sz) return MAXMIN_ERR_DTYPE;
+  if (!in || (!out_max && !out_min)) return MAXMIN_ERR_NULL;
+  if (w_x < 1 || w_y < 1 || w_z < 1) return MAXMIN_ERR_WINDOW;
+  if (depth < 1 || rows < 1 || cols < 1) return MAXMIN_ERR_SHAPE;
+  if (w_x > cols || w_y > rows || w_z > depth) return MAXMIN_ERR_WINDOW_TOO_LARGE;
+  const int64_t D = depth - w_z + 1, R = rows - w_y + 1, C = cols - w_x + 1;
+  if (in_ld < cols || out_ld < C || in_slice < rows * in_ld || (D > 1 && out_slice < R * out_ld))
+    return MAXMIN_ERR_SHAPE;
+  size_t need = 0;
+  int rc = maxmin_filter_3d_workspace_bytes(dt, depth, rows, cols, in_ld, w_z, &need);
+  if (rc != MAXMIN_OK) return rc;
+  size_t t1, t2, ib, ob;
+  if (!extent(rows, cols, in_ld, sz, &t1) || !extent(R, C, out_ld, sz, &t2)) return MAXMIN_ERR_SHAPE;
+  if (!extent(depth, (int64_t)(t1 / sz), in_slice, sz, &ib) || !extent(D, (int64_t)(t2 / sz), D > 1 ? out_slice : 0, sz, &ob))
+    return MAXMIN_ERR_SHAPE;
+  auto el = [sz](const void *p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) % sz) == 0; };
+  if (!el(in) || !el(out_max) || !el(out_min)) return MAXMIN_ERR_ALIGNMENT;
+  if (!workspace || workspace_bytes < need || !aligned16(workspace)) return MAXMIN_ERR_WORKSPACE;
+  const void *regs[4] = {in, out_max, out_min, workspace};
+  const size_t rb[4] = {ib, ob, ob, need};
+  for (int i = 0; i < 4; ++i)
+    for (int k = i + 1; k < 4; ++k)
+      if (regs[i] && regs[k] && overlap(regs[i], rb[i], regs[k], rb[k])) return MAXMIN_ERR_ALIAS;
+  if ((rc = ensure_device(in)) != MAXMIN_OK) return rc;
+  if (out_max && (rc = ensure_device(out_max)) != MAXMIN_OK) return rc;
+  if (out_min && (rc = ensure_device(out_min)) != MAXMIN_OK) return rc;
+  if ((rc = ensure_device(workspace)) != MAXMIN_OK) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  MM_DISPATCH(dt, return mm::launch_3d<T>(in, depth, rows, cols, in_ld, in_slice, w_x, w_y, w_z, out_max, out_min,
+                                          out_ld, out_slice, workspace, s))
+}
+
 // ------------------------------------------------------------ host pipeline
 static int64_t default_chunk(int64_t chunk) { return chunk > 0 ? chunk : (int64_t(1) << 24); }
 

@@ -156,3 +156,19 @@ def test_stream_argument_errors(L):
     assert L.maxmin_stream_push(ctypes.byref(st), None, 9, 0, None, None, 8, ctypes.byref(fv), None) == 5
     assert L.maxmin_stream_push(ctypes.byref(st), None, -1, 0, None, None, 8, ctypes.byref(fv), None) == 5
     assert L.maxmin_stream_push(ctypes.byref(st), None, 1, 0, None, None, 8, None, None) == 1
+
+
+def test_3d_argument_errors(L):
+    b = ctypes.c_size_t(0)
+    assert L.maxmin_filter_3d_workspace_bytes(8, 10, 20, 30, 32, 3, ctypes.byref(b)) == 0 and b.value >= 2 * 8 * 640 * 4
+    assert L.maxmin_filter_3d_workspace_bytes(8, 10, 20, 30, 29, 3, ctypes.byref(b)) == 5  # in_ld < cols
+    assert L.maxmin_filter_3d_workspace_bytes(8, 10, 20, 30, 32, 11, ctypes.byref(b)) == 4
+    f = L.maxmin_filter_3d
+    P = 1 << 30
+    assert f(8, None, 10, 20, 30, 32, 640, 3, 3, 3, P + (1 << 24), None, 28, 560, P + (1 << 26), 1 << 20, None) == 1
+    assert f(8, P, 10, 20, 30, 32, 640, 0, 3, 3, P + (1 << 24), None, 28, 560, P + (1 << 26), 1 << 20, None) == 3
+    assert f(8, P, 10, 20, 30, 32, 640, 31, 3, 3, P + (1 << 24), None, 28, 560, P + (1 << 26), 1 << 20, None) == 4
+    assert f(8, P, 10, 20, 30, 32, 600, 3, 3, 3, P + (1 << 24), None, 28, 560, P + (1 << 26), 1 << 20, None) == 5
+    assert f(8, P, 10, 20, 30, 32, 640, 3, 3, 3, P + (1 << 24) + 2, None, 28, 560, P + (1 << 26), 1 << 20, None) == 6
+    assert f(8, P, 10, 20, 30, 32, 640, 3, 3, 3, P + (1 << 24), None, 28, 560, None, 0, None) == 8
+    assert f(8, P, 10, 20, 30, 32, 640, 3, 3, 3, P + 64, None, 28, 560, P + (1 << 26), 1 << 20, None) == 7

@@ -661,3 +661,26 @@ def test_keogh_rows_shorter_than_pitch(cuda_device):
     lb = mm.maxmin_lb_keogh_batched(torch.from_numpy(c).to(dev()), torch.from_numpy(q).to(dev()), 30, n=1000)
     ref = oracle.keogh(np.ascontiguousarray(c[:, :1000]), q, 30)
     _keogh_close(lb, ref)
+
+
+# ------------------------------------------------------------ N4: 3-D boxes
+@pytest.mark.parametrize("dtype", [np.uint8, np.float32, np.int64, np.float64], ids=lambda d: np.dtype(d).name)
+@pytest.mark.parametrize("wx,wy,wz", [(1, 1, 1), (3, 3, 3), (5, 2, 4), (15, 15, 5), (1, 7, 9), (16, 16, 2)])
+def test_3d_boxes(cuda_device, dtype, wx, wy, wz):
+    a = synth.random_values(np.dtype(dtype), 12 * 40 * 50, seed=wx * 100 + wy * 10 + wz).reshape(12, 40, 50)
+    x = torch.from_numpy(a).to(dev())
+    mx, mn = mm.maxmin_filter_3d(x, wx, wy, wz)
+    torch.cuda.synchronize()
+    ex, en = oracle.separable_3d(a, wx, wy, wz)
+    assert_same(mx, ex, "3d max")
+    assert_same(mn, en, "3d min")
+
+
+def test_3d_strided_and_single_output(cuda_device):
+    a = synth.random_values(np.dtype(np.uint8), 9 * 33 * 64, seed=3).reshape(9, 33, 64)
+    x = torch.from_numpy(a).to(dev())
+    mx, mn = mm.maxmin_filter_3d(x, 4, 5, 3, cols=57, want_min=False)
+    torch.cuda.synchronize()
+    assert mn is None
+    ex, _ = oracle.separable_3d(np.ascontiguousarray(a[:, :, :57]), 4, 5, 3)
+    assert_same(mx, ex, "3d strided max")
