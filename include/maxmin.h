@@ -234,6 +234,23 @@ int maxmin_stream_push(maxmin_stream *st, const void *chunk, int64_t c, int64_t 
                        void *stream);
 
 /*
+ * maxmin_filter_2d with scratch: the same operation and rules, routed to the
+ * fastest applicable path -- the fused packed-byte kernel (1-byte pixels,
+ * square windows <= 17, 16-B aligned rows), else the separable streaming
+ * passes (rows by the 1-D kernels into two scratch images, then a streaming
+ * column pass: w_col <= 16, w_row <= 8193, 16-B aligned input rows, and
+ * `workspace` of maxmin_filter_2d_workspace_bytes -- 0 for 1-byte pixels with
+ * square windows <= 17), else the fused generic kernel.  workspace may be
+ * NULL (then no separable path).
+ */
+int maxmin_filter_2d_workspace_bytes(int dt, int64_t batch, int64_t rows, int64_t cols,
+                                     int64_t w_row, int64_t w_col, size_t *bytes);
+int maxmin_filter_2d_ws(int dt, const void *in, int64_t batch, int64_t rows, int64_t cols,
+                        int64_t in_ld, int64_t in_bstride, int64_t w_row, int64_t w_col,
+                        void *out_max, void *out_min, int64_t out_ld, int64_t out_bstride,
+                        void *workspace, size_t workspace_bytes, void *stream);
+
+/*
  * Grayscale opening and closing (the image-processing use
  * of the filter: erosion = the min filter, dilation = the max
  * filter).  The flat structuring element (w samples; a w_col x w_row
@@ -274,13 +291,15 @@ int maxmin_morph_2d(int dt, const void *in, int64_t batch, int64_t rows, int64_t
  * (cols-w_x+1); outputs with row pitch out_ld and slice pitch out_slice
  * (either output may be NULL).  Element alignment suffices.  Device
  * workspace of maxmin_filter_3d_workspace_bytes (two scratch volumes of D'
- * slices).  Runs as the 2-D kernel along depth (slices as rows, window
- * 1 x w_z), then the 2-D filter (w_x, w_y) of every scratch slice.
+ * slices, plus the row images of the separable 2-D pass).  Runs as a
+ * streaming column pass along depth (w_z <= 16; else the 2-D kernel with
+ * slices as rows), then the 2-D filter (w_x, w_y) of every scratch slice.
  * MAXMIN_ERR_UNSUPPORTED when the depth window exceeds the 2-D kernel's
  * shared memory (about w_z > 140 for 4-byte types).
  */
 int maxmin_filter_3d_workspace_bytes(int dt, int64_t depth, int64_t rows, int64_t cols,
-                                     int64_t in_ld, int64_t w_z, size_t *bytes);
+                                     int64_t in_ld, int64_t w_x, int64_t w_y, int64_t w_z,
+                                     size_t *bytes);
 int maxmin_filter_3d(int dt, const void *in, int64_t depth, int64_t rows, int64_t cols,
                      int64_t in_ld, int64_t in_slice, int64_t w_x, int64_t w_y, int64_t w_z,
                      void *out_max, void *out_min, int64_t out_ld, int64_t out_slice,

@@ -122,8 +122,15 @@ def maxmin_filter_batched(x: torch.Tensor, w: int, n: int | None = None, out_max
     return out_max, out_min
 
 
+@functools.lru_cache(maxsize=256)
+def _workspace_2d(code: int, batch: int, rows: int, cols: int, w_row: int, w_col: int) -> int:
+    out = ctypes.c_size_t(0)
+    _lib.check(_lib.lib().maxmin_filter_2d_workspace_bytes(code, batch, rows, cols, w_row, w_col, ctypes.byref(out)))
+    return int(out.value)
+
+
 def maxmin_filter_2d(x: torch.Tensor, w_row: int, w_col: int, cols: int | None = None, out_max=None,
-                     out_min=None, *, want_max=True, want_min=True, stream=None):
+                     out_min=None, *, want_max=True, want_min=True, workspace=None, stream=None):
     """Separable 2-D max/min over a [batch, rows, ld] (or [rows, ld]) CUDA tensor.
 
     Output (b, r, c) covers rows [r, r+w_col) x columns [c, c+w_row); only the valid
@@ -147,9 +154,14 @@ def maxmin_filter_2d(x: torch.Tensor, w_row: int, w_col: int, cols: int | None =
         om = om[None]
     out_ld = om.stride(1) if om is not None else 1
     out_bs = om.stride(0) if om is not None else 1
-    _lib.check(_lib.lib().maxmin_filter_2d(dtype_code(x.dtype), _ptr(xx), batch, rows, cols,
-                                           xx.stride(1), xx.stride(0), w_row, w_col, _ptr(out_max),
-                                           _ptr(out_min), out_ld, out_bs, _stream_ptr(stream)))
+    need = _workspace_2d(dtype_code(x.dtype), batch, rows, cols, w_row, w_col) if R > 0 and C > 0 else 0
+    if workspace is None and need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+    _lib.check(_lib.lib().maxmin_filter_2d_ws(dtype_code(x.dtype), _ptr(xx), batch, rows, cols,
+                                              xx.stride(1), xx.stride(0), w_row, w_col, _ptr(out_max),
+                                              _ptr(out_min), out_ld, out_bs, _ptr(workspace),
+                                              0 if workspace is None else workspace.numel(),
+                                              _stream_ptr(stream, x.device)))
     if squeeze:
         out_max = out_max[0] if out_max is not None and out_max.dim() == 3 else out_max
         out_min = out_min[0] if out_min is not None and out_min.dim() == 3 else out_min
@@ -349,8 +361,8 @@ def maxmin_filter_3d(x: torch.Tensor, w_x: int, w_y: int, w_z: int, cols: int | 
         out_min = torch.empty(D, R, C, dtype=x.dtype, device=x.device)
     o = out_max if out_max is not None else out_min
     need = ctypes.c_size_t(0)
-    _lib.check(_lib.lib().maxmin_filter_3d_workspace_bytes(dtype_code(x.dtype), depth, rows, cols, x.stride(1), w_z,
-                                                           ctypes.byref(need)))
+    _lib.check(_lib.lib().maxmin_filter_3d_workspace_bytes(dtype_code(x.dtype), depth, rows, cols, x.stride(1), w_x,
+                                                           w_y, w_z, ctypes.byref(need)))
     if workspace is None:
         workspace = torch.empty(max(need.value, 16), dtype=torch.uint8, device=x.device)
     _lib.check(_lib.lib().maxmin_filter_3d(

@@ -70,8 +70,12 @@ SIGNATURES = {
                                                        ctypes.POINTER(_sz)]),
     "maxmin_morph_2d": (ctypes.c_int, [ctypes.c_int, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp,
                                        _i64, _i64, _vp, _sz, _vp]),
-    "maxmin_filter_3d_workspace_bytes": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i64, _i64, _i64,
+    "maxmin_filter_3d_workspace_bytes": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i64, _i64, _i64, _i64, _i64,
                                                         ctypes.POINTER(_sz)]),
+    "maxmin_filter_2d_workspace_bytes": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i64, _i64, _i64,
+                                                        ctypes.POINTER(_sz)]),
+    "maxmin_filter_2d_ws": (ctypes.c_int, [ctypes.c_int, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _i64,
+                                           _vp, _vp, _i64, _i64, _vp, _sz, _vp]),
     "maxmin_filter_3d": (ctypes.c_int, [ctypes.c_int, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp,
                                         _i64, _i64, _vp, _sz, _vp]),
     "maxmin_host_workspace_bytes": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i64, ctypes.POINTER(_sz)]),

@@ -1,0 +1,90 @@
+// kcol.cuh -- the running max-min filter down columns, streaming (used by the
+// separable 2-D path, sep2d.cu, and the depth pass of the 3-D filter,
+// filter3d.cu).
+//
+// A thread owns one column j of `items` columns (image b = j / span, column
+// j % span) and walks down its `depth` elements (pitch `slice`) in blocks of
+// W (compile time, <= 16): van Herk / Gil-Werman along the column -- the
+// block's suffix extrema and the next block's running prefix in registers, so
+// every element is read once and every output written once, coalesced across
+// the warp's adjacent columns.  The max chain reads srcx and the min chain
+// srcn (the same array for a plain filter; the row-max and row-min images for
+// the second pass of a separable filter).
+#pragma once
+
+#include "common.cuh"
+
+namespace mm {
+
+template <typename T, int W>
+__global__ void __launch_bounds__(256) k_col(const T *__restrict__ srcx, const T *__restrict__ srcn, int64_t items,
+                                             int64_t span, int64_t in_bs, int64_t slice, int64_t depth,
+                                             T *__restrict__ omax, T *__restrict__ omin, int64_t out_bs,
+                                             int64_t oslice) {
+  const int64_t D = depth - W + 1;
+  const bool same = srcx == srcn;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items; it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = it / span, j = it - b * span;
+    const T *ax = srcx + b * in_bs + j;
+    const T *an = srcn + b * in_bs + j;
+    T *ox_ = omax ? omax + b * out_bs + j : nullptr;
+    T *on_ = omin ? omin + b * out_bs + j : nullptr;
+    T sx[W], sn[W];  // suffix max / min of the current block
+#pragma unroll
+    for (int t = 0; t < W; ++t) {  // block 0 (W <= depth)
+      sx[t] = ax[(int64_t)t * slice];
+      sn[t] = same ? sx[t] : an[(int64_t)t * slice];
+    }
+#pragma unroll
+    for (int t = W - 2; t >= 0; --t) {
+      sx[t] = Ord<T>::mx(sx[t], sx[t + 1]);
+      sn[t] = Ord<T>::mn(sn[t], sn[t + 1]);
+    }
+    for (int64_t b0 = 0; b0 < D; b0 += W) {  // outputs b0 .. b0+W-1: block b and block b+1
+      T vx[W], vn[W];
+#pragma unroll
+      for (int t = 0; t < W; ++t) {
+        const int64_t z = b0 + W + t;
+        vx[t] = z < depth ? ax[z * slice] : T(0);
+        vn[t] = same ? vx[t] : (z < depth ? an[z * slice] : T(0));
+      }
+      T px = vx[0], pn = vn[0];  // after step t: the next block's prefix over [0, t]
+#pragma unroll
+      for (int t = 0; t < W; ++t) {
+        const int64_t z0 = b0 + t;  // window [z0, z0 + W): block b's suffix from t, next block's [0, t)
+        if (z0 < D) {
+          T x = sx[t], n = sn[t];
+          if (t > 0) {
+            x = Ord<T>::mx(x, px);
+            n = Ord<T>::mn(n, pn);
+          }
+          if (ox_) ox_[z0 * oslice] = x;
+          if (on_) on_[z0 * oslice] = n;
+        }
+        if (t > 0) {
+          px = Ord<T>::mx(px, vx[t]);
+          pn = Ord<T>::mn(pn, vn[t]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < W; ++t) {  // the next block's suffixes
+        sx[t] = vx[t];
+        sn[t] = vn[t];
+      }
+#pragma unroll
+      for (int t = W - 2; t >= 0; --t) {
+        sx[t] = Ord<T>::mx(sx[t], sx[t + 1]);
+        sn[t] = Ord<T>::mn(sn[t], sn[t + 1]);
+      }
+    }
+  }
+}
+
+constexpr int kColMaxW = 16;
+
+// kErrUnsupported (= 10, launch.cuh) for windows longer than kColMaxW
+template <typename T>
+int launch_col(const T *srcx, const T *srcn, int64_t batch, int64_t span, int64_t in_bs, int64_t slice,
+               int64_t depth, int64_t w, T *omax, T *omin, int64_t out_bs, int64_t oslice, int sms, cudaStream_t s);
+
+}  // namespace mm

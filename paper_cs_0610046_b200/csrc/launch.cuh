@@ -70,9 +70,22 @@ StreamLayout stream_layout(int64_t streams, int64_t w, int64_t max_chunk);
 template <typename T>
 int launch_stream_push(void *state, const StreamLayout &L, int64_t streams, int64_t w, int phase, const T *chunk,
                        int64_t c, int64_t chunk_ld, T *out_max, T *out_min, int64_t out_ld, cudaStream_t s);
+// separable 2-D path (sep2d.cu): rows by the 1-D kernels, columns streaming
+template <typename T>
+size_t sep2d_workspace(int64_t batch, int64_t rows, int64_t cols, int64_t w_row, int64_t w_col);
+template <typename T>
+int launch_2d_sep(const void *in, int64_t batch, int64_t rows, int64_t cols, int64_t in_ld, int64_t in_bstride,
+                  int64_t w_row, int64_t w_col, void *out_max, void *out_min, int64_t out_ld, int64_t out_bstride,
+                  void *ws, size_t ws_bytes, cudaStream_t s);
+// the fastest applicable 2-D path: packed bytes, else separable (workspace), else fused generic
+template <typename T>
+int launch_2d_best(const void *in, int64_t batch, int64_t rows, int64_t cols, int64_t in_ld, int64_t in_bstride,
+                   int64_t w_row, int64_t w_col, void *out_max, void *out_min, int64_t out_ld, int64_t out_bstride,
+                   void *ws, size_t ws_bytes, cudaStream_t s);
 // 3-D boxes (filter3d.cu)
 template <typename T>
-size_t filter3d_workspace(int64_t depth, int64_t rows, int64_t cols, int64_t in_ld, int64_t w_z);
+size_t filter3d_workspace(int64_t depth, int64_t rows, int64_t cols, int64_t in_ld, int64_t w_x, int64_t w_y,
+                          int64_t w_z);
 template <typename T>
 int launch_3d(const void *in, int64_t depth, int64_t rows, int64_t cols, int64_t in_ld, int64_t in_slice,
               int64_t w_x, int64_t w_y, int64_t w_z, void *out_max, void *out_min, int64_t out_ld, int64_t out_slice,

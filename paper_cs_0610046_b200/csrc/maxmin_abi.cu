@@ -440,9 +440,11 @@ int maxmin_argfilter_batched(int dt, const void *in, int64_t batch, int64_t n, i
   }
 }
 
-int maxmin_filter_2d(int dt, const void *in, int64_t batch, int64_t rows, int64_t cols, int64_t in_ld,
-                     int64_t in_bstride, int64_t w_row, int64_t w_col, void *out_max, void *out_min,
-                     int64_t out_ld, int64_t out_bstride, void *stream) {
+namespace {
+// argument checks of the 2-D calls; ib / ob: byte extents of the input and of one output
+int validate_2d(int dt, const void *in, int64_t batch, int64_t rows, int64_t cols, int64_t in_ld,
+                int64_t in_bstride, int64_t w_row, int64_t w_col, const void *out_max, const void *out_min,
+                int64_t out_ld, int64_t out_bstride, size_t *ib, size_t *ob) {
   const size_t sz = maxmin_dtype_size(dt);
   if (!sz) return MAXMIN_ERR_DTYPE;
   if (!in || (!out_max && !out_min)) return MAXMIN_ERR_NULL;
@@ -452,10 +454,10 @@ int maxmin_filter_2d(int dt, const void *in, int64_t batch, int64_t rows, int64_
   const int64_t R = rows - w_col + 1, C = cols - w_row + 1;
   if (in_ld < cols || out_ld < C) return MAXMIN_ERR_SHAPE;
   if (batch > 1 && (in_bstride < rows * in_ld || out_bstride < R * out_ld)) return MAXMIN_ERR_SHAPE;
-  size_t ib, ob, t1, t2;
+  size_t t1, t2;
   if (!extent(rows, cols, in_ld, sz, &t1) || !extent(R, C, out_ld, sz, &t2)) return MAXMIN_ERR_SHAPE;
-  if (!extent(batch, (int64_t)(t1 / sz), batch > 1 ? in_bstride : 0, sz, &ib) ||
-      !extent(batch, (int64_t)(t2 / sz), batch > 1 ? out_bstride : 0, sz, &ob))
+  if (!extent(batch, (int64_t)(t1 / sz), batch > 1 ? in_bstride : 0, sz, ib) ||
+      !extent(batch, (int64_t)(t2 / sz), batch > 1 ? out_bstride : 0, sz, ob))
     return MAXMIN_ERR_SHAPE;
   // 2-D copies each box row separately (16-B aligned outward), so only element
   // alignment is required of pointers and strides.
@@ -463,16 +465,80 @@ int maxmin_filter_2d(int dt, const void *in, int64_t batch, int64_t rows, int64_
   if (!el_aligned(in) || (out_max && !el_aligned(out_max)) || (out_min && !el_aligned(out_min)))
     return MAXMIN_ERR_ALIGNMENT;
   if (batch == 0) return MAXMIN_OK;
-  if (out_max && overlap(in, ib, out_max, ob)) return MAXMIN_ERR_ALIAS;
-  if (out_min && overlap(in, ib, out_min, ob)) return MAXMIN_ERR_ALIAS;
-  if (out_max && out_min && overlap(out_max, ob, out_min, ob)) return MAXMIN_ERR_ALIAS;
-  int rc;
+  if (out_max && overlap(in, *ib, out_max, *ob)) return MAXMIN_ERR_ALIAS;
+  if (out_min && overlap(in, *ib, out_min, *ob)) return MAXMIN_ERR_ALIAS;
+  if (out_max && out_min && overlap(out_max, *ob, out_min, *ob)) return MAXMIN_ERR_ALIAS;
+  return MAXMIN_OK;
+}
+}  // namespace
+
+int maxmin_filter_2d(int dt, const void *in, int64_t batch, int64_t rows, int64_t cols, int64_t in_ld,
+                     int64_t in_bstride, int64_t w_row, int64_t w_col, void *out_max, void *out_min,
+                     int64_t out_ld, int64_t out_bstride, void *stream) {
+  size_t ib = 0, ob = 0;
+  int rc = validate_2d(dt, in, batch, rows, cols, in_ld, in_bstride, w_row, w_col, out_max, out_min, out_ld,
+                       out_bstride, &ib, &ob);
+  if (rc != MAXMIN_OK || batch == 0) return rc;
   if ((rc = ensure_device(in)) != MAXMIN_OK) return rc;
   if (out_max && (rc = ensure_device(out_max)) != MAXMIN_OK) return rc;
   if (out_min && (rc = ensure_device(out_min)) != MAXMIN_OK) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   MM_DISPATCH(dt, return mm::launch_2d<T>(in, batch, rows, cols, in_ld, in_bstride, w_row, w_col,
                                           out_max, out_min, out_ld, out_bstride, s))
+}
+
+int maxmin_filter_2d_workspace_bytes(int dt, int64_t batch, int64_t rows, int64_t cols, int64_t w_row, int64_t w_col,
+                                     size_t *bytes) {
+  if (!bytes) return MAXMIN_ERR_NULL;
+  *bytes = 0;
+  const size_t sz = maxmin_dtype_size(dt);
+  if (!sz) return MAXMIN_ERR_DTYPE;
+  if (w_row < 1 || w_col < 1) return MAXMIN_ERR_WINDOW;
+  if (batch < 0 || rows < 1 || cols < 1) return MAXMIN_ERR_SHAPE;
+  if (w_row > cols || w_col > rows) return MAXMIN_ERR_WINDOW_TOO_LARGE;
+  size_t t;
+  if (!extent(batch > 0 ? batch : 1, rows * (cols + 16), rows * (cols + 16), sz, &t)) return MAXMIN_ERR_SHAPE;
+  // 1-byte pixels in the packed kernel's domain need no scratch (its alignment
+  // rules aside: an unaligned call falls back to the fused generic kernel)
+  if (sz == 1 && w_row == w_col && w_row <= 17) return MAXMIN_OK;
+  MM_DISPATCH(dt, { *bytes = mm::sep2d_workspace<T>(batch, rows, cols, w_row, w_col); return MAXMIN_OK; })
+}
+
+int maxmin_filter_2d_ws(int dt, const void *in, int64_t batch, int64_t rows, int64_t cols, int64_t in_ld,
+                        int64_t in_bstride, int64_t w_row, int64_t w_col, void *out_max, void *out_min,
+                        int64_t out_ld, int64_t out_bstride, void *workspace, size_t workspace_bytes, void *stream) {
+  size_t ib = 0, ob = 0;
+  int rc = validate_2d(dt, in, batch, rows, cols, in_ld, in_bstride, w_row, w_col, out_max, out_min, out_ld,
+                       out_bstride, &ib, &ob);
+  if (rc != MAXMIN_OK || batch == 0) return rc;
+  size_t need = 0;
+  if ((rc = maxmin_filter_2d_workspace_bytes(dt, batch, rows, cols, w_row, w_col, &need)) != MAXMIN_OK) return rc;
+  if (workspace && !aligned16(workspace)) return MAXMIN_ERR_WORKSPACE;
+  const size_t wsb = workspace ? workspace_bytes : 0;
+  if (workspace && wsb) {
+    if (overlap(workspace, wsb, in, ib) || (out_max && overlap(workspace, wsb, out_max, ob)) ||
+        (out_min && overlap(workspace, wsb, out_min, ob)))
+      return MAXMIN_ERR_ALIAS;
+  }
+  if ((rc = ensure_device(in)) != MAXMIN_OK) return rc;
+  if (out_max && (rc = ensure_device(out_max)) != MAXMIN_OK) return rc;
+  if (out_min && (rc = ensure_device(out_min)) != MAXMIN_OK) return rc;
+  if (workspace && wsb && (rc = ensure_device(workspace)) != MAXMIN_OK) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // the fused packed-byte kernel, else the separable streaming passes (when the
+  // workspace suffices), else the fused generic kernel
+  if (maxmin_dtype_size(dt) == 1) {
+    rc = mm::launch_2d_byte(dt == MAXMIN_I8, in, batch, rows, cols, in_ld, in_bstride, w_row, w_col, out_max, out_min,
+                            out_ld, out_bstride, s);
+    if (rc != MAXMIN_ERR_UNSUPPORTED) return rc;
+  }
+  MM_DISPATCH(dt, {
+    rc = mm::launch_2d_sep<T>(in, batch, rows, cols, in_ld, in_bstride, w_row, w_col, out_max, out_min, out_ld,
+                              out_bstride, workspace, wsb, s);
+    if (rc != MAXMIN_ERR_UNSUPPORTED) return rc;
+    return mm::launch_2d<T>(in, batch, rows, cols, in_ld, in_bstride, w_row, w_col, out_max, out_min, out_ld,
+                            out_bstride, s);
+  })
 }
 
 // ------------------------------------------------------------ N2: streams
@@ -646,18 +712,21 @@ int maxmin_morph_2d(int dt, const void *in, int64_t batch, int64_t rows, int64_t
 }
 
 // ------------------------------------------------------------ N4: 3-D boxes
-int maxmin_filter_3d_workspace_bytes(int dt, int64_t depth, int64_t rows, int64_t cols, int64_t in_ld, int64_t w_z,
-                                     size_t *bytes) {
+int maxmin_filter_3d_workspace_bytes(int dt, int64_t depth, int64_t rows, int64_t cols, int64_t in_ld, int64_t w_x,
+                                     int64_t w_y, int64_t w_z, size_t *bytes) {
   if (!bytes) return MAXMIN_ERR_NULL;
   *bytes = 0;
   const size_t sz = maxmin_dtype_size(dt);
   if (!sz) return MAXMIN_ERR_DTYPE;
-  if (w_z < 1) return MAXMIN_ERR_WINDOW;
+  if (w_x < 1 || w_y < 1 || w_z < 1) return MAXMIN_ERR_WINDOW;
   if (depth < 1 || rows < 1 || cols < 1 || in_ld < cols) return MAXMIN_ERR_SHAPE;
-  if (w_z > depth) return MAXMIN_ERR_WINDOW_TOO_LARGE;
+  if (w_z > depth || w_x > cols || w_y > rows) return MAXMIN_ERR_WINDOW_TOO_LARGE;
   size_t t;
   if (!extent(depth, rows * in_ld + 16, rows * in_ld + 16, sz, &t)) return MAXMIN_ERR_SHAPE;
-  MM_DISPATCH(dt, { *bytes = mm::filter3d_workspace<T>(depth, rows, cols, in_ld, w_z); return MAXMIN_OK; })
+  MM_DISPATCH(dt, {
+    *bytes = mm::filter3d_workspace<T>(depth, rows, cols, in_ld, w_x, w_y, w_z);
+    return MAXMIN_OK;
+  })
 }
 
 int maxmin_filter_3d(int dt, const void *in, int64_t depth, int64_t rows, int64_t cols, int64_t in_ld,
@@ -673,7 +742,7 @@ int maxmin_filter_3d(int dt, const void *in, int64_t depth, int64_t rows, int64_
   if (in_ld < cols || out_ld < C || in_slice < rows * in_ld || (D > 1 && out_slice < R * out_ld))
     return MAXMIN_ERR_SHAPE;
   size_t need = 0;
-  int rc = maxmin_filter_3d_workspace_bytes(dt, depth, rows, cols, in_ld, w_z, &need);
+  int rc = maxmin_filter_3d_workspace_bytes(dt, depth, rows, cols, in_ld, w_x, w_y, w_z, &need);
   if (rc != MAXMIN_OK) return rc;
   size_t t1, t2, ib, ob;
   if (!extent(rows, cols, in_ld, sz, &t1) || !extent(R, C, out_ld, sz, &t2)) return MAXMIN_ERR_SHAPE;

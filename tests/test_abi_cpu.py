@@ -160,9 +160,9 @@ def test_stream_argument_errors(L):
 
 def test_3d_argument_errors(L):
     b = ctypes.c_size_t(0)
-    assert L.maxmin_filter_3d_workspace_bytes(8, 10, 20, 30, 32, 3, ctypes.byref(b)) == 0 and b.value >= 2 * 8 * 640 * 4
-    assert L.maxmin_filter_3d_workspace_bytes(8, 10, 20, 30, 29, 3, ctypes.byref(b)) == 5  # in_ld < cols
-    assert L.maxmin_filter_3d_workspace_bytes(8, 10, 20, 30, 32, 11, ctypes.byref(b)) == 4
+    assert L.maxmin_filter_3d_workspace_bytes(8, 10, 20, 30, 32, 3, 3, 3, ctypes.byref(b)) == 0 and b.value >= 2 * 8 * 640 * 4
+    assert L.maxmin_filter_3d_workspace_bytes(8, 10, 20, 30, 29, 3, 3, 3, ctypes.byref(b)) == 5  # in_ld < cols
+    assert L.maxmin_filter_3d_workspace_bytes(8, 10, 20, 30, 32, 3, 3, 11, ctypes.byref(b)) == 4
     f = L.maxmin_filter_3d
     P = 1 << 30
     assert f(8, None, 10, 20, 30, 32, 640, 3, 3, 3, P + (1 << 24), None, 28, 560, P + (1 << 26), 1 << 20, None) == 1
