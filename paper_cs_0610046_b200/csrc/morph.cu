@@ -431,7 +431,7 @@ template <typename T>
 struct Morph2DLayout {  // workspace: [padded e | padded d | (1-byte types) aligned e | aligned d]
   int64_t PR, PC, ld, bs;  // padded frames
   int64_t R, C, eld, ebs;  // aligned valid-region buffers
-  size_t frame, valid, total;
+  size_t frame, valid, sep, total;
   Morph2DLayout(int64_t batch, int64_t rows, int64_t cols, int64_t w_row, int64_t w_col) {
     constexpr int VEC = 16 / (int)sizeof(T);
     auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -445,7 +445,11 @@ struct Morph2DLayout {  // workspace: [padded e | padded d | (1-byte types) alig
     eld = (C + VEC - 1) / VEC * VEC;
     ebs = R * eld;
     valid = sizeof(T) == 1 ? up((size_t)batch * ebs) : 0;
-    total = 2 * frame + 2 * valid;
+    // the separable 2-D path's row images (the larger of the two passes' needs)
+    const size_t s1 = sep2d_workspace<T>(batch, rows, cols, w_row, w_col);
+    const size_t s2 = sep2d_workspace<T>(batch, PR, PC, w_row, w_col);
+    sep = up(s1 > s2 ? s1 : s2);
+    total = 2 * frame + 2 * valid + sep;
   }
 };
 
@@ -472,13 +476,15 @@ int launch_morph_2d(const void *in, int64_t batch, int64_t rows, int64_t cols, i
     if (rc) return rc;
   }
   const int64_t off = (w_col - 1) * L.ld + (w_row - 1);
+  void *sepws = base + 2 * L.frame + 2 * L.valid;
   int rc;
   if (sizeof(T) == 1) {
     // the packed byte kernel writes 4-B aligned rows only: e and d go to aligned
     // buffers first, then into the frames' (unaligned) interiors
     T *ve = reinterpret_cast<T *>(base + 2 * L.frame);
     T *vd = reinterpret_cast<T *>(base + 2 * L.frame + L.valid);
-    rc = launch_2d<T>(in, batch, rows, cols, in_ld, in_bstride, w_row, w_col, vd, ve, L.eld, L.ebs, s);
+    rc = launch_2d_best<T>(in, batch, rows, cols, in_ld, in_bstride, w_row, w_col, vd, ve, L.eld, L.ebs, sepws, L.sep,
+                           s);
     if (rc) return rc;
     const int64_t items = 2 * batch * L.R;
     const int64_t blocks = std::min<int64_t>((items + 7) / 8, (int64_t)sm_count() * 16);
@@ -487,16 +493,19 @@ int launch_morph_2d(const void *in, int64_t batch, int64_t rows, int64_t cols, i
         reinterpret_cast<const uint8_t *>(ve), reinterpret_cast<const uint8_t *>(vd), L.eld, L.ebs,
         reinterpret_cast<uint8_t *>(pe + off), reinterpret_cast<uint8_t *>(pd + off), L.ld, L.bs, batch, L.R, L.C, D);
     rc = note_cuda(cudaGetLastError());
-  } else {  // the generic 2-D kernel stores at any element alignment
-    rc = launch_2d<T>(in, batch, rows, cols, in_ld, in_bstride, w_row, w_col, pd + off, pe + off, L.ld, L.bs, s);
+  } else {  // the separable and the generic 2-D paths store at any element alignment
+    rc = launch_2d_best<T>(in, batch, rows, cols, in_ld, in_bstride, w_row, w_col, pd + off, pe + off, L.ld, L.bs,
+                           sepws, L.sep, s);
   }
   if (rc) return rc;
   if (out_open) {
-    rc = launch_2d<T>(pe, batch, L.PR, L.PC, L.ld, L.bs, w_row, w_col, out_open, nullptr, out_ld, out_bstride, s);
+    rc = launch_2d_best<T>(pe, batch, L.PR, L.PC, L.ld, L.bs, w_row, w_col, out_open, nullptr, out_ld, out_bstride,
+                           sepws, L.sep, s);
     if (rc) return rc;
   }
   if (out_close)
-    rc = launch_2d<T>(pd, batch, L.PR, L.PC, L.ld, L.bs, w_row, w_col, nullptr, out_close, out_ld, out_bstride, s);
+    rc = launch_2d_best<T>(pd, batch, L.PR, L.PC, L.ld, L.bs, w_row, w_col, nullptr, out_close, out_ld, out_bstride,
+                           sepws, L.sep, s);
   return rc;
 }
 
