@@ -2,9 +2,10 @@
 // separable 2-D path, sep2d.cu, and the depth pass of the 3-D filter,
 // filter3d.cu).
 //
-// A thread owns one column j of `items` columns (image b = j / span, column
-// j % span) and walks down its `depth` elements (pitch `slice`) in blocks of
-// W (compile time, <= 16): van Herk / Gil-Werman along the column -- the
+// A thread owns one column j (image b, column j % span) over a segment of
+// `seg` outputs -- columns alone give too few threads for an image -- and
+// walks down its elements (pitch `slice`) in blocks of W (compile time, <= 16;
+// a segment re-reads the W-1 rows before its end): van Herk / Gil-Werman along the column -- the
 // block's suffix extrema and the next block's running prefix in registers, so
 // every element is read once and every output written once, coalesced across
 // the warp's adjacent columns.  The max chain reads srcx and the min chain
@@ -18,29 +19,33 @@ namespace mm {
 
 template <typename T, int W>
 __global__ void __launch_bounds__(256) k_col(const T *__restrict__ srcx, const T *__restrict__ srcn, int64_t items,
-                                             int64_t span, int64_t in_bs, int64_t slice, int64_t depth,
+                                             int64_t span, int64_t in_bs, int64_t slice, int64_t depth, int64_t seg,
                                              T *__restrict__ omax, T *__restrict__ omin, int64_t out_bs,
                                              int64_t oslice) {
   const int64_t D = depth - W + 1;
+  const int64_t nseg = (D + seg - 1) / seg;
   const bool same = srcx == srcn;
   for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items; it += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = it / span, j = it - b * span;
+    // item = (segment, image, column), column fastest: a warp reads adjacent columns
+    const int64_t sg = it / (items / nseg), rest = it - sg * (items / nseg);
+    const int64_t b = rest / span, j = rest - b * span;
+    const int64_t zb = sg * seg, ze = zb + seg < D ? zb + seg : D;  // outputs [zb, ze)
     const T *ax = srcx + b * in_bs + j;
     const T *an = srcn + b * in_bs + j;
     T *ox_ = omax ? omax + b * out_bs + j : nullptr;
     T *on_ = omin ? omin + b * out_bs + j : nullptr;
     T sx[W], sn[W];  // suffix max / min of the current block
 #pragma unroll
-    for (int t = 0; t < W; ++t) {  // block 0 (W <= depth)
-      sx[t] = ax[(int64_t)t * slice];
-      sn[t] = same ? sx[t] : an[(int64_t)t * slice];
+    for (int t = 0; t < W; ++t) {  // the block [zb, zb + W) (zb + W <= depth)
+      sx[t] = ax[(zb + t) * slice];
+      sn[t] = same ? sx[t] : an[(zb + t) * slice];
     }
 #pragma unroll
     for (int t = W - 2; t >= 0; --t) {
       sx[t] = Ord<T>::mx(sx[t], sx[t + 1]);
       sn[t] = Ord<T>::mn(sn[t], sn[t + 1]);
     }
-    for (int64_t b0 = 0; b0 < D; b0 += W) {  // outputs b0 .. b0+W-1: block b and block b+1
+    for (int64_t b0 = zb; b0 < ze; b0 += W) {  // outputs b0 .. b0+W-1: block b and block b+1
       T vx[W], vn[W];
 #pragma unroll
       for (int t = 0; t < W; ++t) {
@@ -52,7 +57,7 @@ __global__ void __launch_bounds__(256) k_col(const T *__restrict__ srcx, const T
 #pragma unroll
       for (int t = 0; t < W; ++t) {
         const int64_t z0 = b0 + t;  // window [z0, z0 + W): block b's suffix from t, next block's [0, t)
-        if (z0 < D) {
+        if (z0 < ze) {
           T x = sx[t], n = sn[t];
           if (t > 0) {
             x = Ord<T>::mx(x, px);

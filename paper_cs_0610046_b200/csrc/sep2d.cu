@@ -19,14 +19,25 @@ namespace mm {
 template <typename T>
 int launch_col(const T *srcx, const T *srcn, int64_t batch, int64_t span, int64_t in_bs, int64_t slice,
                int64_t depth, int64_t w, T *omax, T *omin, int64_t out_bs, int64_t oslice, int sms, cudaStream_t s) {
-  const int64_t items = batch * span;
-  if (items == 0) return kOK;
+  const int64_t cols_total = batch * span;
+  if (cols_total == 0) return kOK;
+  const int64_t D = depth - w + 1;
+  // segments of outputs per column: enough threads to fill the GPU (~64 K), each
+  // segment >= 64 outputs so the W-1 re-read rows stay a small overhead
+  int64_t seg = D;
+  const int64_t want = (int64_t)sms * 512;
+  if (cols_total < want) {
+    const int64_t nseg = (want + cols_total - 1) / cols_total;
+    seg = (D + nseg - 1) / nseg;
+    if (seg < 64) seg = 64;
+  }
+  const int64_t items = cols_total * ((D + seg - 1) / seg);
   const int64_t blocks = std::min<int64_t>((items + 255) / 256, (int64_t)sms * 8);
   const int g = (int)(blocks > 0 ? blocks : 1);
   switch (w) {
-#define MM_COL_CASE(W)                                                                                        \
-  case W:                                                                                                     \
-    k_col<T, W><<<g, 256, 0, s>>>(srcx, srcn, items, span, in_bs, slice, depth, omax, omin, out_bs, oslice); \
+#define MM_COL_CASE(W)                                                                                             \
+  case W:                                                                                                          \
+    k_col<T, W><<<g, 256, 0, s>>>(srcx, srcn, items, span, in_bs, slice, depth, seg, omax, omin, out_bs, oslice); \
     return note_cuda(cudaGetLastError());
     MM_COL_CASE(1) MM_COL_CASE(2) MM_COL_CASE(3) MM_COL_CASE(4) MM_COL_CASE(5) MM_COL_CASE(6) MM_COL_CASE(7)
     MM_COL_CASE(8) MM_COL_CASE(9) MM_COL_CASE(10) MM_COL_CASE(11) MM_COL_CASE(12) MM_COL_CASE(13)
