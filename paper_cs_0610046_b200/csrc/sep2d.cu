@@ -31,6 +31,29 @@ int launch_col(const T *srcx, const T *srcn, int64_t batch, int64_t span, int64_
     seg = (D + nseg - 1) / nseg;
     if (seg < 64) seg = 64;
   }
+  if constexpr (sizeof(T) == 1) {  // four columns per thread, packed (k_col_b8)
+    auto al4 = [](const void *p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 3) == 0; };
+    if (span % 4 == 0 && in_bs % 4 == 0 && slice % 4 == 0 && out_bs % 4 == 0 && oslice % 4 == 0 && al4(srcx) &&
+        al4(srcn) && al4(omax) && al4(omin)) {
+      const int64_t items4 = cols_total / 4 * ((D + seg - 1) / seg);
+      const int64_t blocks4 = std::min<int64_t>((items4 + 255) / 256, (int64_t)sms * 8);
+      const int g4 = (int)(blocks4 > 0 ? blocks4 : 1);
+      constexpr bool SG = std::is_signed<T>::value;
+      const uint8_t *ux = reinterpret_cast<const uint8_t *>(srcx), *un = reinterpret_cast<const uint8_t *>(srcn);
+      uint8_t *qx = reinterpret_cast<uint8_t *>(omax), *qn = reinterpret_cast<uint8_t *>(omin);
+      switch (w) {
+#define MM_COLB_CASE(W)                                                                                           \
+  case W:                                                                                                         \
+    k_col_b8<W, SG><<<g4, 256, 0, s>>>(ux, un, items4, span / 4, in_bs, slice, depth, seg, qx, qn, out_bs, oslice); \
+    return note_cuda(cudaGetLastError());
+        MM_COLB_CASE(1) MM_COLB_CASE(2) MM_COLB_CASE(3) MM_COLB_CASE(4) MM_COLB_CASE(5) MM_COLB_CASE(6)
+        MM_COLB_CASE(7) MM_COLB_CASE(8) MM_COLB_CASE(9) MM_COLB_CASE(10) MM_COLB_CASE(11) MM_COLB_CASE(12)
+        MM_COLB_CASE(13) MM_COLB_CASE(14) MM_COLB_CASE(15) MM_COLB_CASE(16)
+#undef MM_COLB_CASE
+        default: return kErrUnsupported;
+      }
+    }
+  }
   const int64_t items = cols_total * ((D + seg - 1) / seg);
   const int64_t blocks = std::min<int64_t>((items + 255) / 256, (int64_t)sms * 8);
   const int g = (int)(blocks > 0 ? blocks : 1);
