@@ -684,3 +684,17 @@ def test_3d_strided_and_single_output(cuda_device):
     assert mn is None
     ex, _ = oracle.separable_3d(np.ascontiguousarray(a[:, :, :57]), 4, 5, 3)
     assert_same(mx, ex, "3d strided max")
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.uint8, np.int16], ids=lambda d: np.dtype(d).name)
+def test_2d_separable_cropped_batch(cuda_device, dtype):
+    """Images cropped from a larger buffer (image stride != rows * row pitch): the
+    separable path's per-image row passes; windows outside the packed-byte domain."""
+    big = synth.random_values(np.dtype(dtype), 3 * 80 * 96, seed=17).reshape(3, 80, 96)
+    x = torch.from_numpy(big).to(dev())[:, 5:69, :]  # 64 rows of each 80-row image: stride 80 * 96
+    for wr, wc in [(5, 3), (1, 9), (12, 16), (33, 2)]:
+        mx, mn = mm.maxmin_filter_2d(x, wr, wc, cols=90)
+        torch.cuda.synchronize()
+        ex, en = oracle.separable_2d(np.ascontiguousarray(big[:, 5:69, :90]), wr, wc)
+        assert_same(mx, ex, f"max {wr}x{wc}")
+        assert_same(mn, en, f"min {wr}x{wc}")
