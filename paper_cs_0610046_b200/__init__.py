@@ -134,7 +134,10 @@ def maxmin_filter_2d(x: torch.Tensor, w_row: int, w_col: int, cols: int | None =
     """Separable 2-D max/min over a [batch, rows, ld] (or [rows, ld]) CUDA tensor.
 
     Output (b, r, c) covers rows [r, r+w_col) x columns [c, c+w_row); only the valid
-    region (rows-w_col+1) x (cols-w_row+1) is computed.
+    region (rows-w_col+1) x (cols-w_row+1) is computed.  Outside the packed-byte
+    kernel's domain (1-byte pixels, square windows <= 17) the separable path needs
+    scratch of two row-filtered images (maxmin_filter_2d_workspace_bytes); pass
+    `workspace` to reuse a buffer, else one is allocated from torch's caching allocator.
     """
     squeeze = x.dim() == 2
     xx = x[None] if squeeze else x
