@@ -34,6 +34,26 @@ def _timed(step, steps, warmup, world, dev):
     return float(t.item()), clk.summary()
 
 
+def _e2e(step, h_in, d_in, d_outs, outs, steps, world, dev, api, unit):
+    """The same metric end to end: every step copies its input from pinned host memory,
+    runs the call and copies its outputs back to pinned host memory."""
+    import torch
+
+    h_outs = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in d_outs]
+
+    def e2e_step():
+        d_in.copy_(h_in, non_blocking=True)
+        step()
+        for h, d in zip(h_outs, d_outs):
+            h.copy_(d, non_blocking=True)
+
+    k = max(1, steps)
+    ms, _ = _timed(e2e_step, k, 1, world, dev)
+    return {"value": outs / (ms / k / 1e3), "unit": unit,
+            "h2d_bytes_per_step": h_in.numel() * h_in.element_size(),
+            "d2h_bytes_per_step": sum(o.numel() * o.element_size() for o in d_outs), "api": api}
+
+
 def run_extra(args, rank, world, local):
     import numpy as np
     import torch
@@ -46,6 +66,7 @@ def run_extra(args, rank, world, local):
     dev = torch.device("cuda", local)
     peak, peak_src = bench.load_peaks()
     e2e = None
+    e2e_io = None  # (pinned host input, device input, device outputs, api) for the e2e leg
     cfg = args.config
     if cfg == "C1":
         n, w = synth.C1["n"], synth.C1["w"]
@@ -69,6 +90,7 @@ def run_extra(args, rank, world, local):
         ms, clk = _timed(step, steps, args.warmup, world, dev)
         sample = host
         windows = (w,)
+        e2e_io = (torch.from_numpy(host).pin_memory(), x, [ox, on], "maxmin_filter_1d")
     elif cfg == "C3":
         B, n, w = synth.C3["batch"], synth.C3["n"], synth.C3["w"]
         r0, r1 = shard.shard_items(B, world, rank)
@@ -99,6 +121,7 @@ def run_extra(args, rank, world, local):
         ms, clk = _timed(step, steps, args.warmup, world, dev)
         sample = host[:2048].numpy()
         windows = (w,)
+        e2e_io = (host, x, [ox, on], "maxmin_filter_batched")
     elif cfg == "C4":
         NI, R, C, w = synth.C4["batch"], synth.C4["rows"], synth.C4["cols"], synth.C4["w_row"]
         i0, i1 = shard.shard_items(NI, world, rank)
@@ -130,6 +153,7 @@ def run_extra(args, rank, world, local):
         ms, clk = _timed(step, steps, args.warmup, world, dev)
         sample = None
         windows = (w,)
+        e2e_io = (host, x, [ox, on], "maxmin_filter_2d")
     elif cfg == "N3":
         # SURVEY.md §8(f) N3 on C3's candidates: LB_Keogh of every series against one
         # query, envelope radius 64 (w = 129), the envelope never leaving the chip
@@ -164,6 +188,7 @@ def run_extra(args, rank, world, local):
         ms, clk = _timed(step, steps, args.warmup, world, dev)
         sample = None
         windows = (w,)
+        e2e_io = (host, x, [lb], "maxmin_lb_keogh_batched")
     elif cfg == "N1":
         # SURVEY.md §8(f) N1 on C2's array: values and earliest positions of the
         # max and min of every window, w = 1024
@@ -208,6 +233,7 @@ def run_extra(args, rank, world, local):
         ms, clk = _timed(step, steps, args.warmup, world, dev)
         sample = None
         windows = (w,)
+        e2e_io = (host, x, [ox, on, ax, an], "maxmin_argfilter_batched")
     elif cfg == "N2":
         # C3's 65 536 series as online streams, w = 129, each step
         # ingests the 4096 samples of every stream in 16 pushes of 256 (every push emits
@@ -303,9 +329,14 @@ def run_extra(args, rank, world, local):
         ms, clk = _timed(step, steps, args.warmup, world, dev)
         sample = None
         windows = (w,)
+        e2e_io = (host, x, [oo, oc], "maxmin_morph_batched")
     else:
         raise SystemExit(f"unknown config {cfg}")
 
+    if e2e is None and e2e_io is not None and not getattr(args, "no_e2e", False):
+        h_in, d_in, d_outs, api = e2e_io
+        e2e = _e2e(step, h_in, d_in, d_outs, outs, max(1, min(steps, 5)), world, dev, api,
+                   "bounds/s" if cfg == "N3" else bench.UNIT)
     ms_step = ms / steps
     value = outs / (ms_step / 1e3)
     unit = "bounds/s" if cfg == "N3" else bench.UNIT
