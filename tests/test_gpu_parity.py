@@ -698,3 +698,31 @@ def test_2d_separable_cropped_batch(cuda_device, dtype):
         ex, en = oracle.separable_2d(np.ascontiguousarray(big[:, 5:69, :90]), wr, wc)
         assert_same(mx, ex, f"max {wr}x{wc}")
         assert_same(mn, en, f"min {wr}x{wc}")
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.uint16, np.int8], ids=lambda d: np.dtype(d).name)
+def test_2d_plain_entry_generic_kernel(cuda_device, dtype):
+    """maxmin_filter_2d (no scratch) through the C ABI: the fused kernels only (packed
+    bytes or the generic 2-D kernel), and maxmin_filter_2d_ws without a workspace."""
+    import ctypes
+
+    a = synth.random_values(np.dtype(dtype), 2 * 60 * 70, seed=44).reshape(2, 60, 70)
+    x = torch.from_numpy(a).to(dev())
+    L = mm._lib.lib()
+    vp = ctypes.c_void_p
+    for wr, wc in [(5, 7), (3, 3), (20, 2)]:
+        R, C = 60 - wc + 1, 70 - wr + 1
+        ex, en = oracle.separable_2d(a, wr, wc)
+        for entry in ("plain", "ws_null"):
+            ox = torch.empty(2, R, C, dtype=x.dtype, device=dev())
+            on = torch.empty_like(ox)
+            args = [mm.dtype_code(x.dtype), vp(x.data_ptr()), 2, 60, 70, 70, 60 * 70, wr, wc, vp(ox.data_ptr()),
+                    vp(on.data_ptr()), C, R * C]
+            stream = vp(torch.cuda.current_stream().cuda_stream)
+            if entry == "plain":
+                mm._lib.check(L.maxmin_filter_2d(*args, stream))
+            else:
+                mm._lib.check(L.maxmin_filter_2d_ws(*args, vp(0), 0, stream))
+            torch.cuda.synchronize()
+            assert_same(ox, ex, f"{entry} max {wr}x{wc}")
+            assert_same(on, en, f"{entry} min {wr}x{wc}")
