@@ -172,3 +172,17 @@ def test_3d_argument_errors(L):
     assert f(8, P, 10, 20, 30, 32, 640, 3, 3, 3, P + (1 << 24) + 2, None, 28, 560, P + (1 << 26), 1 << 20, None) == 6
     assert f(8, P, 10, 20, 30, 32, 640, 3, 3, 3, P + (1 << 24), None, 28, 560, None, 0, None) == 8
     assert f(8, P, 10, 20, 30, 32, 640, 3, 3, 3, P + 64, None, 28, 560, P + (1 << 26), 1 << 20, None) == 7
+
+
+def test_2d_ws_argument_errors(L):
+    b = ctypes.c_size_t(0)
+    assert L.maxmin_filter_2d_workspace_bytes(8, 2, 100, 120, 5, 7, ctypes.byref(b)) == 0 and b.value >= 2 * 2 * 100 * 116 * 4
+    assert L.maxmin_filter_2d_workspace_bytes(0, 2, 100, 120, 15, 15, ctypes.byref(b)) == 0 and b.value == 0  # packed bytes
+    assert L.maxmin_filter_2d_workspace_bytes(8, 2, 100, 120, 5, 17, ctypes.byref(b)) == 0 and b.value == 0  # w_col > 16
+    assert L.maxmin_filter_2d_workspace_bytes(8, 2, 100, 120, 0, 7, ctypes.byref(b)) == 3
+    assert L.maxmin_filter_2d_workspace_bytes(8, 2, 100, 120, 121, 7, ctypes.byref(b)) == 4
+    f = L.maxmin_filter_2d_ws
+    P = 1 << 30
+    assert f(8, None, 1, 10, 10, 16, 160, 3, 3, P + (1 << 20), None, 16, 160, None, 0, None) == 1
+    assert f(8, P, 1, 10, 10, 16, 160, 3, 3, P + (1 << 20), None, 16, 160, P + (1 << 24) + 4, 1 << 20, None) == 8
+    assert f(8, P, 1, 10, 10, 16, 160, 3, 3, P + 32, None, 16, 160, None, 0, None) == 7
