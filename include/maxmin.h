@@ -192,10 +192,9 @@ int maxmin_lb_keogh_batched(int dt, const void *cand, int64_t batch, int64_t n,
  * State: device memory of maxmin_stream_state_bytes(...) bytes, 16-byte
  * aligned, owned by the caller, described by a host-side maxmin_stream that
  * maxmin_stream_init fills in (it also zero-fills the device state on
- * `stream`).  Per stream it holds the last w-1 samples (for E <= w-1 <= 1024,
- * E = 16 elements, 8 for 8-byte types: two ping-pong rows, and a push is ONE
- * kernel; otherwise a [history | max_chunk slot] row plus filter scratch, and
- * a push is copy-in, filter, shift).  The struct is the caller's; push
+ * `stream`).  Per stream it holds the last w-1 samples (for w-1 <= 1024: two
+ * ping-pong rows, and a push is ONE kernel; otherwise a [history | max_chunk
+ * slot] row plus filter scratch, and a push is copy-in, filter, shift).  The struct is the caller's; push
  * updates `seen` and `phase`.
  *
  * maxmin_stream_push(st, chunk, c, chunk_ld, out_max, out_min, out_ld,

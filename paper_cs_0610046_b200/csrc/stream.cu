@@ -11,7 +11,7 @@
 //
 // Two paths, chosen by w when the state is created:
 //
-// fused (E <= w-1 <= kStreamHMax; k_stream_fused): ONE kernel per push reads
+// fused (w-1 <= kStreamHMax; k_stream_fused): ONE kernel per push reads
 //   each stream's history and its new chunk, writes the c windows and the new
 //   history -- exactly the algorithmic bytes: c + 2c + 2(w-1) per stream.
 //   History rows are kept right-aligned in ping-pong buffers of hld =
@@ -25,7 +25,7 @@
 //   the far blocks before the segment are reduced from the staged halo.  The
 //   warp holding a stream's last window writes the new history.
 //
-// composed (any other w): the state row is [history (w-1) | slot (max_chunk)];
+// composed (w-1 > kStreamHMax): the state row is [history (w-1) | slot (max_chunk)];
 //   a push copies the chunk into the slot, runs the batched filter (any 1-D
 //   kernel) over [0, w-1+c) and moves the last w-1 samples to the front.
 //   HBM bytes: 2c + (w-1+c) + 2c + 2(w-1) per stream.
@@ -225,7 +225,10 @@ __global__ void __launch_bounds__(32 * kStreamWarps) k_stream_fused(StreamArgs a
     const int64_t left = a.c - j0;
     const int cnt = left < SEG ? (int)left : SEG;
     T ox[E], on[E];
-    warp_window_med<T, E, G>(PairLoader<T>{X}, P, a.g, agg, lane, ox, on);
+    if constexpr (G == 0)  // w <= E: log-step doubling + barrel shift
+      warp_window_small<T, E>(PairLoader<T>{X}, P, w, lane, ox, on);
+    else
+      warp_window_med<T, E, G>(PairLoader<T>{X}, P, a.g, agg, lane, ox, on);
     const int c0 = lane * E;
     if (c0 < cnt) {
       T *omx = a.out_max ? static_cast<T *>(a.out_max) + row * a.out_ld + j0 + c0 : nullptr;
@@ -272,7 +275,7 @@ StreamLayout stream_layout(int64_t streams, int64_t w, int64_t max_chunk) {
   constexpr int VEC = 16 / (int)sizeof(T);
   auto up256 = [](size_t x) { return (x + 255) & ~size_t(255); };
   StreamLayout L;
-  L.fused = (w - 1 >= Chunk<T>::E && w - 1 <= kStreamHMax) ? 1 : 0;
+  L.fused = (w - 1 <= kStreamHMax) ? 1 : 0;
   if (L.fused) {  // two history buffers (ping-pong), rows right-aligned
     L.ld = (w - 1 + VEC - 1) / VEC * VEC;
     L.hist_bytes = up256((size_t)streams * L.ld * sizeof(T));
@@ -293,8 +296,12 @@ int launch_fused_g(StreamArgs a, cudaStream_t s) {
   a.segs_per_row = (a.c + Geo::SEG - 1) / Geo::SEG;
   a.nseg = a.streams * a.segs_per_row;
   if (a.nseg > 0x7fffffffLL) return kErrUnsupported;
-  a.g = make_warp_geom<E>(a.w, G);
-  if (a.g.V + 32 / G > WarpAgg<T>::AGG) return kErrUnsupported;
+  if constexpr (G > 0) {
+    a.g = make_warp_geom<E>(a.w, G);
+    if (a.g.V + 32 / G > WarpAgg<T>::AGG) return kErrUnsupported;
+  } else {
+    a.g.w = a.w;
+  }
   // staging depth: the most segments in flight per SM
   WarpLaunch L;
   int rc = warp_launch_choice(reinterpret_cast<const void *>(k_stream_fused<T, E, G>), a.w, kStreamWarps, kStreamWarps,
@@ -334,6 +341,10 @@ int launch_stream_push(void *state, const StreamLayout &L, int64_t streams, int6
     a.w = (int)w;
     a.P = (int)(L.ld - h);
     a.chunk_vec = (reinterpret_cast<uintptr_t>(chunk) % 16 == 0 && (chunk_ld * (int64_t)sizeof(T)) % 16 == 0) ? 1 : 0;
+    if (h < EB) {  // w <= E: the small-window path
+      if (ES < EB && c <= 32 * ES && h < ES) return launch_fused_g<T, ES, 0>(a, s);
+      return launch_fused_g<T, EB, 0>(a, s);
+    }
     const bool small_e = ES < EB && c <= 32 * ES && h >= ES;
     if (small_e) {
       switch (warp_group<ES>(w)) {
