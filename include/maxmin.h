@@ -260,8 +260,9 @@ int maxmin_filter_2d_ws(int dt, const void *in, int64_t batch, int64_t rows, int
  *
  * maxmin_morph_batched: rows b of in + b*in_ld (n samples each); out_open /
  *   out_close (either may be NULL) rows at pitch out_ld, 16-byte aligned with
- *   16-byte row pitch; in needs element alignment.  w - 1 <= 1024 (else
- *   MAXMIN_ERR_UNSUPPORTED).  One fused kernel: the input is read once and
+ *   16-byte row pitch; in needs element alignment.  w - 1 <= 8192 (else
+ *   MAXMIN_ERR_UNSUPPORTED; 8-byte types stop where a warp's staging no longer
+ *   fits shared memory, about w - 1 <= 4000).  One fused kernel: the input is read once and
  *   each output written once.  No workspace.
  * maxmin_morph_2d: images as maxmin_filter_2d; outputs [batch][rows][cols]
  *   with pitch out_ld / out_bstride, element alignment.  Device workspace of

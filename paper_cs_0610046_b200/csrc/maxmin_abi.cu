@@ -644,7 +644,7 @@ int maxmin_morph_batched(int dt, const void *in, int64_t batch, int64_t n, int64
   if (w < 1) return MAXMIN_ERR_WINDOW;
   if (n < 1 || batch < 0) return MAXMIN_ERR_SHAPE;
   if (w > n) return MAXMIN_ERR_WINDOW_TOO_LARGE;
-  if (w - 1 > 1024) return MAXMIN_ERR_UNSUPPORTED;
+  if (w - 1 > 8192) return MAXMIN_ERR_UNSUPPORTED;  // (and when the staging does not fit shared memory)
   if (in_ld < n || out_ld < n) return MAXMIN_ERR_SHAPE;
   size_t ib, ob;
   if (!extent(batch, n, in_ld, sz, &ib) || !extent(batch, n, out_ld, sz, &ob)) return MAXMIN_ERR_SHAPE;

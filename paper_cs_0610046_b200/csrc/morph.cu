@@ -33,7 +33,7 @@
 namespace mm {
 
 constexpr int kMorphWarps = 4;
-constexpr int kMorphHMax = 1024;  // largest w-1 of k_morph_fused
+constexpr int kMorphHMax = 8192;  // largest w-1 of k_morph_fused (past ~1024 a warp stages w-1 twice: few warps fit)
 
 template <typename T>
 __device__ __forceinline__ T lowest_value() {

@@ -544,7 +544,7 @@ def test_stream_c3_full_size(cuda_device):
 
 
 # ------------------------------------------------------------- N4: morphology
-MORPH_W = [1, 2, 3, 5, 8, 15, 16, 17, 18, 31, 33, 64, 129, 200, 513, 600, 1025]
+MORPH_W = [1, 2, 3, 5, 8, 15, 16, 17, 18, 31, 33, 64, 129, 200, 513, 600, 1025, 1026, 3000, 8193]
 
 
 @pytest.mark.parametrize("w", MORPH_W)
