@@ -15,30 +15,35 @@
 
 #include "common.cuh"
 
+#ifndef MM_COL_MINB
+#define MM_COL_MINB 2  // 16 warps per SM for <= 4-byte types (8-byte types: 1, they would spill)
+#endif
+
 namespace mm {
 
 template <typename T, int W>
-__global__ void __launch_bounds__(256) k_col(const T *__restrict__ srcx, const T *__restrict__ srcn, int64_t items,
-                                             int64_t span, int64_t in_bs, int64_t slice, int64_t depth, int64_t seg,
-                                             T *__restrict__ omax, T *__restrict__ omin, int64_t out_bs,
-                                             int64_t oslice) {
+__global__ void __launch_bounds__(256, (sizeof(T) >= 8 ? 1 : MM_COL_MINB)) k_col(const T *__restrict__ srcx, const T *__restrict__ srcn,
+                                                          int64_t items, int64_t span, int64_t in_bs, int64_t slice,
+                                                          int64_t depth, int64_t seg, T *__restrict__ omax,
+                                                          T *__restrict__ omin, int64_t out_bs, int64_t oslice) {
   const int64_t D = depth - W + 1;
   const int64_t nseg = (D + seg - 1) / seg;
   const bool same = srcx == srcn;
+  const int64_t dn = srcn - srcx;  // the min chain's source, relative to the max chain's
   for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items; it += (int64_t)gridDim.x * blockDim.x) {
     // item = (segment, image, column), column fastest: a warp reads adjacent columns
     const int64_t sg = it / (items / nseg), rest = it - sg * (items / nseg);
     const int64_t b = rest / span, j = rest - b * span;
     const int64_t zb = sg * seg, ze = zb + seg < D ? zb + seg : D;  // outputs [zb, ze)
-    const T *ax = srcx + b * in_bs + j;
-    const T *an = srcn + b * in_bs + j;
-    T *ox_ = omax ? omax + b * out_bs + j : nullptr;
-    T *on_ = omin ? omin + b * out_bs + j : nullptr;
+    // running pointers (one 64-bit register each instead of an address per row)
+    const T *pin = srcx + b * in_bs + j + zb * slice;
+    T *pox = omax ? omax + b * out_bs + j + zb * oslice : nullptr;
+    T *pon = omin ? omin + b * out_bs + j + zb * oslice : nullptr;
     T sx[W], sn[W];  // suffix max / min of the current block
 #pragma unroll
-    for (int t = 0; t < W; ++t) {  // the block [zb, zb + W) (zb + W <= depth)
-      sx[t] = ax[(zb + t) * slice];
-      sn[t] = same ? sx[t] : an[(zb + t) * slice];
+    for (int t = 0; t < W; ++t, pin += slice) {  // the block [zb, zb + W) (zb + W <= depth)
+      sx[t] = pin[0];
+      sn[t] = same ? sx[t] : pin[dn];
     }
 #pragma unroll
     for (int t = W - 2; t >= 0; --t) {
@@ -47,24 +52,30 @@ __global__ void __launch_bounds__(256) k_col(const T *__restrict__ srcx, const T
     }
     for (int64_t b0 = zb; b0 < ze; b0 += W) {  // outputs b0 .. b0+W-1: block b and block b+1
       T vx[W], vn[W];
+      const int64_t avail = depth - (b0 + W);  // rows of block b+1 inside the column
 #pragma unroll
-      for (int t = 0; t < W; ++t) {
-        const int64_t z = b0 + W + t;
-        vx[t] = z < depth ? ax[z * slice] : T(0);
-        vn[t] = same ? vx[t] : (z < depth ? an[z * slice] : T(0));
+      for (int t = 0; t < W; ++t, pin += slice) {
+        vx[t] = t < avail ? pin[0] : T(0);
+        vn[t] = same ? vx[t] : (t < avail ? pin[dn] : T(0));
       }
-      T px = vx[0], pn = vn[0];  // after step t: the next block's prefix over [0, t]
+      const int64_t nout = ze - b0;  // outputs of this block still in the segment
+      T px = vx[0], pn = vn[0];      // after step t: the next block's prefix over [0, t]
 #pragma unroll
-      for (int t = 0; t < W; ++t) {
-        const int64_t z0 = b0 + t;  // window [z0, z0 + W): block b's suffix from t, next block's [0, t)
-        if (z0 < ze) {
+      for (int t = 0; t < W; ++t) {  // window [b0 + t, b0 + t + W): block b's suffix from t, next block's [0, t)
+        if (t < nout) {
           T x = sx[t], n = sn[t];
           if (t > 0) {
             x = Ord<T>::mx(x, px);
             n = Ord<T>::mn(n, pn);
           }
-          if (ox_) ox_[z0 * oslice] = x;
-          if (on_) on_[z0 * oslice] = n;
+          if (pox) {
+            *pox = x;
+            pox += oslice;
+          }
+          if (pon) {
+            *pon = n;
+            pon += oslice;
+          }
         }
         if (t > 0) {
           px = Ord<T>::mx(px, vx[t]);
