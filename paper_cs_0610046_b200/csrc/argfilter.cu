@@ -12,17 +12,18 @@
 //                                                   the smallest position
 // with ord() an order-preserving map of the <= 4-byte element type to uint32
 // (floats: the sign-magnitude flip; +-0 both map to +0's code, reading R8).
-// Three steps, all on the GPU: keys (elementwise), the max filter on kx and
-// the min filter on kn (k1d_small/medium/large<uint64_t>), decode
-// (elementwise).  The keys and the key outputs live in the workspace: ~92 B of
-// HBM traffic per element.
-//
-// Fused path (w-1 <= kArgHMax, aligned outputs; k_arg_fused): the keys never
-// reach memory.  Warp-autonomous like the stream and morphology kernels
-// (kwarp.cuh): a warp stages the raw values of its 256 windows plus the w-1
-// halo with cp.async and builds both keys on the fly inside the loads
-// (ArgLoader), so the traffic is the contract's: the input once, the values
-// and the int64 positions out once (4n + 24m bytes for f32).
+// Paths, in order of preference (the keys never reach memory in the first two):
+//   * 8 < w <= 8193, 16-B aligned input rows: k1d_medium itself on 64-bit keys
+//     with a source policy (ArgSrc: TMA stages the raw values, the loads build
+//     both keys with their row positions) and a decoding epilogue (ArgEpi):
+//     the contract's traffic, 4n + 24m bytes for f32;
+//   * w-1 <= kArgHMax: the warp-autonomous kernel (k_arg_fused, kwarp.cuh),
+//     cp.async staging, keys built in the loads (ArgLoader) -- small windows
+//     and unaligned rows;
+//   * otherwise the composition: keys (elementwise), the max filter on kx and
+//     the min filter on kn (the 8-byte 1-D kernels), decode (elementwise); the
+//     keys and the key outputs live in the workspace, ~92 B of HBM traffic per
+//     element.
 #include "kwarp.cuh"
 #include "launch.cuh"
 
