@@ -2,15 +2,23 @@
 """Bench harness: the running max-min filter on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {cuda,reference}]
-                    [--config {C2,C3,C4,C5,C1}]
+                    [--config {C2,C5,C1,C3,C4,N1,N2,N3,N4}]
 
-Default workload (BASELINE.json configs[1], C2): a 1-D fp32 random walk of
-n = 2^28 elements per GPU; one step = the filter for every window of the config
+Default workload (BASELINE.json configs[1], C2): ONE 1-D fp32 random walk of
+n = 2^28 elements; one step = the filter for every window of the config
 (w = 3, 32, 1024, 65536), i.e. every kernel path (small, medium, large) over the
 same HBM-resident input.  value = output elements (2 per window: max and min)
-of all ranks per second.  For N > 1 each rank owns a 2^28 chunk of an N*2^28
-array and receives the next rank's first w_max-1 elements by NCCL (weak
-scaling).  The other configs (C1, C3, C4, C5) are available with --config.
+of all ranks per second.
+
+N > 1 (strong scaling): the same global array is cut
+into contiguous chunks, c_r = r * floor(n/N) aligned down to 256 elements; rank
+r holds its chunk plus a (w_max-1)-element halo slot and computes every window
+that starts in its chunk through maxmin_filter_1d_sharded (the C ABI): the
+halo -- rank r+1's first w_max-1 elements -- arrives by one NCCL send/recv pair
+per boundary on a comm stream while the interior windows run.  `--gpus N`
+without torchrun spawns the N ranks itself (torch.distributed.run, one GPU per
+rank, 127.0.0.1).  C5 (n = 2^30) is sharded the same way; C1/C3/C4/N* shard
+by item (bench_extra.py).
 
 Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement".
 """
@@ -19,7 +27,9 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -29,6 +39,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "max-min filter output elements/s and HBM GB/s vs peak at 1/2/4/8 B200"
 UNIT = "output elements/s"
+NOMINAL_HBM_GBS = 8000.0  # B200 HBM3e nominal (B200_PROFILING.md: 8 TB/s DGX); context denominator
 
 
 # ----------------------------------------------------------------- helpers --
@@ -42,6 +53,14 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def roofline(achieved_gbs: float, traffic, kernel: str, note: str):
+    peak, src = load_peaks()
+    return {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s", "frac": achieved_gbs / peak,
+            "traffic": traffic, "kernel": kernel, "peak_source": src,
+            "peak_nominal": NOMINAL_HBM_GBS, "frac_nominal": achieved_gbs / NOMINAL_HBM_GBS,
+            "algorithmic_bytes": note}
+
+
 def ncu_traffic(config: str, kernel_w):
     """dram bytes per launch of the dominant kernel from the committed ncu capture."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -53,7 +72,10 @@ def ncu_traffic(config: str, kernel_w):
 
 
 class ClockSampler:
-    """Samples SM clock + clock-event reasons via NVML while the timed region runs."""
+    """Samples SM clock + clock-event reasons via NVML (every ~2 ms) from before
+    the warm-up until the timed region ends; the summary covers the samples taken
+    under load: a soak of untimed steps right before the timed region and the
+    timed region itself (mark() brackets them)."""
 
     REASONS = {
         0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
@@ -61,10 +83,11 @@ class ClockSampler:
         0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
     }
 
-    def __init__(self, index: int, period_s: float = 0.005):
+    def __init__(self, index: int, period_s: float = 0.002):
         self.index, self.period = index, period_s
-        self.samples, self.reasons = [], set()
+        self.samples = []  # (t, mhz, reason mask)
         self.max_mhz = None
+        self.windows = []  # [t0, t1) regions under load
         self._stop = threading.Event()
         self._t = None
         try:
@@ -82,11 +105,10 @@ class ClockSampler:
         nv = self.nv
         while not self._stop.is_set():
             try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                t = time.perf_counter()
+                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
                 mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if mask & bit and name != "gpu_idle":
-                        self.reasons.add(name)
+                self.samples.append((t, mhz, mask))
             except Exception:
                 pass
             time.sleep(self.period)
@@ -102,71 +124,124 @@ class ClockSampler:
         if self._t is not None:
             self._t.join()
 
+    def mark(self, t0: float, t1: float):
+        self.windows.append((t0, t1))
+
     def summary(self):
         if self.nv is None:
             return {"error": getattr(self, "err", "nvml unavailable")}
-        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.samples)}
+        inside = [(mhz, mask) for t, mhz, mask in self.samples if any(a <= t < b for a, b in self.windows)]
+        reasons = set()
+        for _, mask in inside:
+            for bit, name in self.REASONS.items():
+                if mask & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median([m for m, _ in inside]) if inside else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons), "samples": len(inside),
+                "window": "soak steps right before the timed region + the timed region"}
 
 
-# -------------------------------------------------------------- workloads ---
+def timed_loop(step, steps: int, stream, clk: ClockSampler, soak_s: float = 0.25):
+    """Untimed soak (>= soak_s of steps, for the clock record) then EXACTLY `steps`
+    steps between two CUDA events on `stream`.  Returns ms."""
+    import torch
+
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < soak_s:
+        step()
+        torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk.mark(t_soak, time.perf_counter())
+    return e0.elapsed_time(e1)
+
 
 def algo_bytes_1d(sz, n, w):
     return sz * (n + 2 * (n - w + 1))
 
 
-def cpu_baseline(config: str, a_sample, windows, dtype_np):
-    """The oracle as it stands (single-threaded appendix variant)
-    on a bounded sample of the same workload."""
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+# ------------------------------------------------------------ CPU baseline --
+
+def cpu_baseline(config: str, a_sample, windows, threads: int | None = None):
+    """The oracle's streaming algorithm (the appendix listing) as it
+    stands, built -O3 -march=native on this host, timed on 1 thread and on all host
+    threads (contiguous window ranges, each with its own (w-1)-element input overlap),
+    best of 2 each, on a bounded sample of the same workload."""
+    import numpy as np
+
     import oracle
 
-    t0 = time.perf_counter()
-    outs = 0
-    for w in windows:
-        mx, mn, _ = oracle.appendix(a_sample, w)
-        outs += 2 * mx.shape[0]
-    dt = time.perf_counter() - t0
-    return {"value": outs / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{config}: first {a_sample.shape[0]} elements of the bench array, "
-                      f"windows {list(windows)}, oracle_appendix (C, gcc -O2, 1 thread), {dt:.2f} s"}
+    allt = oracle.host_threads() if threads is None else threads
+    n = a_sample.shape[0]
+    outs = sum(2 * (n - w + 1) for w in windows)
+    res = {}
+    for th in sorted({1, allt}):
+        bufs = {w: (np.empty(n - w + 1, a_sample.dtype), np.empty(n - w + 1, a_sample.dtype)) for w in windows}
+        best = None
+        for _ in range(2):  # the first pass also pre-faults the output pages
+            t0 = time.perf_counter()
+            for w in windows:
+                oracle.appendix_baseline(a_sample, w, th, *bufs[w])
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        res[th] = outs / best
+    return {"value": res[allt], "unit": UNIT, "cores": allt, "kind": "oracle",
+            "value_1thread": res[1],
+            "sample": f"{config}: first {n} elements of the bench array, windows {list(windows)}; "
+                      f"oracle_appendix (gcc {' '.join(oracle.NATIVE_FLAGS)}), {allt} threads "
+                      f"(contiguous window ranges) and 1 thread, best of 2"}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the oracle (the tier's reference arm) on the host cores."""
-    import numpy as np
-
-    import synth
-
+    """--impl reference: the oracle (the tier's reference arm) on the host cores,
+    rank 0 only; the other ranks exit without work."""
     if rank != 0:
         return
-    cfg = args.config
+    import numpy as np
+
+    import oracle
+
+    cfg = args.config if args.config in CONFIGS else "C2"
     windows = CONFIGS[cfg]["windows"]
     sample_n = CONFIGS[cfg]["ref_sample"]
     a = CONFIGS[cfg]["gen_sample"](sample_n)
-    import oracle
+    th = oracle.host_threads()
+    bufs = {w: (np.empty(sample_n - w + 1, a.dtype), np.empty(sample_n - w + 1, a.dtype)) for w in windows}
+
+    def step():
+        for w in windows:
+            oracle.appendix_baseline(a, w, th, *bufs[w])
 
     for _ in range(args.warmup):
-        oracle.appendix(a[: min(sample_n, 1 << 16)], windows[0])
+        step()
     times = []
-    outs = 0
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        o = 0
-        for w in windows:
-            mx, mn, _ = oracle.appendix(a, w) if a.ndim == 1 else (None, None, None)
-            o += 2 * mx.shape[0]
+        step()
         times.append(time.perf_counter() - t0)
-        outs = o
-    step = statistics.median(times)
-    v = outs / step
+    outs = sum(2 * (sample_n - w + 1) for w in windows)
+    step_s = statistics.median(times)
+    v = outs / step_s
+    sample = (f"first {sample_n} elements of {cfg}'s array, windows {list(windows)} per step; oracle_appendix "
+              f"(gcc {' '.join(oracle.NATIVE_FLAGS)}) on {th} host threads, contiguous window ranges; "
+              f"value = outputs / median step time")
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": {"workload": CONFIGS[cfg]["name"] + " (bounded sample)",
                                             "sample_elements": int(sample_n)},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"first {sample_n} elements, windows {list(windows)}"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": th, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -184,215 +259,285 @@ def _gen_c5(n):
 
 
 CONFIGS = {
-    "C2": dict(name="C2: 1-D fp32 random walk, n=2^28 per GPU, w in {3,32,1024,65536}",
+    "C2": dict(name="C2: 1-D fp32 random walk, n=2^28 (one array; N>1: contiguous chunks + (w-1) NCCL halo), "
+                    "w in {3,32,1024,65536}",
                n=1 << 28, windows=(3, 32, 1024, 65536), gen="c2", ref_sample=1 << 24,
                gen_sample=_gen_c2),
-    "C5": dict(name="C5: 1-D fp32 adversarial mix, n=2^30, w in {7,4096,262144}",
+    "C5": dict(name="C5: 1-D fp32 adversarial mix, n=2^30 (one array; N>1: contiguous chunks + (w-1) NCCL halo), "
+                    "w in {7,4096,262144}",
                n=1 << 30, windows=(7, 4096, 262144), gen="c5", ref_sample=1 << 24,
                gen_sample=_gen_c5),
 }
+EXTRA = ("C1", "C3", "C4", "N1", "N2", "N3", "N4")
 
 
-def main():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS) + ["C1", "C3", "C4", "N1", "N2", "N3", "N4"])
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS) + list(EXTRA))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    args = ap.parse_args()
+    ap.add_argument("--spawn-check", action="store_true",
+                    help="start the ranks, report them and exit (tests the launcher; gloo without a GPU)")
+    args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3) if args.impl == "cuda" else args.warmup
+    return args
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+
+def spawn_ranks(args_argv, n: int) -> int:
+    """`--gpus N` outside torchrun: start N ranks with torch.distributed.run on this
+    node (127.0.0.1, a free port), one GPU each; rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *args_argv]
+    return subprocess.call(cmd)
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse_args(argv)
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0:
+        if args.gpus > 1 and not (args.impl == "reference"):
+            sys.exit(spawn_ranks(argv, args.gpus))
+        world = 1
+    elif world != args.gpus and args.impl == "cuda":
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; refusing to report another count")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
-        if args.config not in CONFIGS:
-            args.config = "C2"
         return run_reference(args, rank, world)
 
     import torch
 
+    if args.spawn_check:
+        return spawn_check(rank, world, local)
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if args.config in ("C1", "C3", "C4", "N1", "N2", "N3", "N4"):
+    if args.config in EXTRA:
         from bench_extra import run_extra
 
         return run_extra(args, rank, world, local)
     return run_1d(args, rank, world, local)
 
 
+def spawn_check(rank, world, local):
+    """Reports the ranks the launcher started (all_gather over gloo or NCCL)."""
+    import torch
+    import torch.distributed as dist
+
+    use_cuda = torch.cuda.is_available()
+    if world > 1:
+        if use_cuda:
+            torch.cuda.set_device(local)
+        dist.init_process_group("nccl" if use_cuda else "gloo")
+        got = [None] * world
+        dist.all_gather_object(got, {"rank": rank, "local": local, "pid": os.getpid()})
+    else:
+        got = [{"rank": 0, "local": local, "pid": os.getpid()}]
+    if rank == 0:
+        print(json.dumps({"spawn_check": True, "world": world, "ranks": got}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def run_1d(args, rank, world, local):
     import numpy as np
     import torch
+    import torch.distributed as dist
 
     import paper_cs_0610046_b200 as mm
     from paper_cs_0610046_b200 import shard
-    import synth
 
     cfg = CONFIGS[args.config]
     windows = cfg["windows"]
-    n_local = cfg["n"]
+    n_total = cfg["n"]
     wmax = max(windows)
-    halo = (wmax - 1) if world > 1 else 0
-    chunk = shard.Chunk1D(rank=rank, world=world, n_local=n_local, halo=halo)
+    bounds = shard.split_even(n_total, world, align=256)
+    c0, c1 = bounds[rank]
+    n_local = c1 - c0
+    halo = wmax - 1 if world > 1 else 0
+    last = rank == world - 1
     dev = torch.device("cuda", local)
 
-    # input: this rank's chunk of the global array, generated on the host (untimed)
-    host = torch.empty(n_local + wmax, dtype=torch.float32).pin_memory()
-    gen = synth.c2 if cfg["gen"] == "c2" else synth.c5
-    gen(n_local, stream=rank, out=host[:n_local].numpy())
-    buf = torch.empty(n_local + wmax, dtype=torch.float32, device=dev)
-    buf.copy_(host)
+    # the global array up to this rank's chunk end + halo, generated on the host
+    # (untimed); this rank's chunk goes to HBM, the halo is what NCCL delivers
+    gen = cfg["gen_sample"]
+    glob_np = gen(min(c1 + halo, n_total))
+    host = torch.empty(n_local + max(halo, 0) + 64, dtype=torch.float32).pin_memory()
+    host[:n_local].copy_(torch.from_numpy(glob_np[c0:c1]))
+    buf = torch.empty(n_local + halo + 64, dtype=torch.float32, device=dev)
+    buf[:n_local].copy_(host[:n_local])
     outs = {}
     for w in windows:
-        m = chunk.windows(w)
-        outs[w] = (torch.empty(m, dtype=torch.float32, device=dev),
-                   torch.empty(m, dtype=torch.float32, device=dev))
-    ws_bytes = max(mm.maxmin_workspace_bytes(torch.float32, 1, n_local + wmax, w) for w in windows)
-    ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
+        m = n_local - w + 1 if last else n_local
+        outs[w] = (torch.empty(m, dtype=torch.float32, device=dev), torch.empty(m, dtype=torch.float32, device=dev))
 
     stream = torch.cuda.current_stream()
+    if world > 1:
+        comm_stream = torch.cuda.Stream(device=dev)
+        comm = shard.nccl_comm_ptr(dev)
+        ws_bytes = mm.maxmin_sharded_workspace_bytes(torch.float32, n_local, halo, windows)
+    else:
+        ws_bytes = max(mm.maxmin_workspace_bytes(torch.float32, 1, n_local, w) for w in windows)
+    ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
     per_w_events = {w: [] for w in windows}
     record = {"on": False}
 
-    def filt(x, w, ox, on):
+    def filt(w):
+        ox, on = outs[w]
         if record["on"]:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            mm.maxmin_filter_1d(x, w, out_max=ox, out_min=on, workspace=ws)
+            mm.maxmin_filter_1d(buf[:n_local], w, out_max=ox[: n_local - w + 1], out_min=on[: n_local - w + 1],
+                                workspace=ws)
             e1.record(stream)
-            per_w_events[w].append((e0, e1, x.shape[0] == n_local))
+            per_w_events[w].append((e0, e1))
         else:
-            mm.maxmin_filter_1d(x, w, out_max=ox, out_min=on, workspace=ws)
+            mm.maxmin_filter_1d(buf[:n_local], w, out_max=ox[: n_local - w + 1], out_min=on[: n_local - w + 1],
+                                workspace=ws)
 
-    def step():
-        if world > 1:
-            shard.filter_1d_sharded(buf, chunk, windows, outs, filt)
-        else:
+    if world > 1:
+        def step():
+            mm.maxmin_filter_1d_sharded(buf, n_local, halo, windows, [outs[w][0] for w in windows],
+                                        [outs[w][1] for w in windows], rank, world, comm, workspace=ws,
+                                        stream=stream, comm_stream=comm_stream)
+    else:
+        def step():
             for w in windows:
-                ox, on = outs[w]
-                filt(buf[:n_local], w, ox, on)
-
-    import torch.distributed as dist
+                filt(w)
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        step()
-    barrier()
-    # parity spot check of this run's outputs (oracle on bounded slices; untimed)
-    parity = spot_check(host[:n_local].numpy(), outs, windows, chunk, rank)
-
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    barrier()
-    record["on"] = True
-    with ClockSampler(local) as clk:
-        t0.record(stream)
-        for _ in range(args.steps):
+    clk = ClockSampler(local)
+    with clk:
+        for _ in range(args.warmup):
             step()
-        t1.record(stream)
-        torch.cuda.synchronize()
-    record["on"] = False
-    ms = t0.elapsed_time(t1)
+        barrier()
+        # bit-exact check of this run's outputs against the oracle (untimed):
+        # slices around tile seams, and at N > 1 every window of the rank seam
+        parity = spot_check(glob_np, c0, n_local, last, outs, windows)
+        if world > 1:
+            ok = torch.tensor([1 if parity["bit_exact"] else 0], device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            cnt = torch.tensor([parity["outputs_checked"], parity["seam_windows_checked"]], device=dev,
+                               dtype=torch.float64)
+            dist.all_reduce(cnt)
+            parity.update(bit_exact=bool(ok.item()), outputs_checked=int(cnt[0].item()),
+                          seam_windows_checked=int(cnt[1].item()), ranks=world)
+        barrier()
+        if world == 1:
+            record["on"] = True
+        ms = timed_loop(step, args.steps, stream, clk)
+        record["on"] = False
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
-    outs_per_step_rank = sum(2 * chunk.windows(w) for w in windows)
-    outs_per_step = torch.tensor([outs_per_step_rank], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(outs_per_step)
-    total_outs = float(outs_per_step.item()) * args.steps
-    value = total_outs / (ms_max / 1e3)
+    outs_per_step = float(sum(2 * (n_total - w + 1) for w in windows))  # every window of the global array
+    value = outs_per_step * args.steps / (ms_max / 1e3)
 
-    # per-window kernel time (CUDA events on the launching stream): the full-chunk
-    # call of each window (the interior call when sharded), averaged per launch
-    peak, peak_src = load_peaks()
+    # per-window kernel time (CUDA events on the launching stream): at N = 1 the
+    # timed region's own launches; at N > 1 the interior calls, timed after it
+    if world > 1:
+        record["on"] = True
+        for _ in range(3):
+            for w in windows:
+                filt(w)
+        torch.cuda.synchronize()
+        record["on"] = False
     per_w = {}
     for w in windows:
-        durs = [a.elapsed_time(b) for a, b, full in per_w_events[w] if full]
+        durs = [a.elapsed_time(b) for a, b in per_w_events[w]]
         d = sum(durs) / len(durs)  # ms per launch
         nb = algo_bytes_1d(4, n_local, w)
         per_w[str(w)] = {"ms_per_launch": d, "algo_bytes": nb, "gbs": nb / (d / 1e3) / 1e9,
-                         "frac_of_peak": nb / (d / 1e3) / 1e9 / peak,
-                         "launches_per_step": len(per_w_events[w]) / args.steps}
+                         "frac_of_peak": nb / (d / 1e3) / 1e9 / load_peaks()[0],
+                         "frac_of_nominal": nb / (d / 1e3) / 1e9 / NOMINAL_HBM_GBS}
     dom = max(windows, key=lambda w: per_w[str(w)]["ms_per_launch"])
-    achieved = per_w[str(dom)]["gbs"]
-    traffic = ncu_traffic(args.config, dom)
 
-    line = None
     if rank == 0:
-        e2e = None if args.no_e2e or world > 1 else run_e2e(args, host, n_local, windows, dev)
-        if world > 1:
-            e2e = {"value": None, "unit": UNIT, "note": "e2e measured at N=1 only",
-                   "h2d_bytes_per_step": None, "d2h_bytes_per_step": None}
+        e2e = None
+        if not args.no_e2e:
+            e2e = run_e2e(args, host, n_local, windows, dev) if world == 1 else \
+                run_e2e_sharded(args, step, host, buf, outs, n_local, windows, dev, world, n_total)
         cpu = None
         if not args.no_cpu and world == 1:
-            cpu = cpu_baseline(args.config, host[: 1 << 26].numpy().copy(), windows, np.float32)
+            cpu = cpu_baseline(args.config, np.ascontiguousarray(glob_np[: 1 << 26]), windows)
+        launches = len(windows) * (1 if world == 1 or last else 2)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["name"], "n_per_gpu": n_local, "windows": list(windows),
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["name"], "n_total": n_total, "n_per_gpu": n_local, "windows": list(windows),
                        "step": "one filter call per window over the whole array (all kernel paths)",
-                       "l2": "inputs (1 GiB per GPU) larger than the 126 MB L2; no flush needed",
-                       "parallelism": f"sequence sharding, contiguous chunks + (w-1) NCCL halo, dp{world}"
-                       if world > 1 else "single GPU"},
-            "hbm_gbs_step": sum(algo_bytes_1d(4, n_local, w) for w in windows) * world
-            / (ms_max / args.steps / 1e3) / 1e9,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": f"w={dom}",
-                         "peak_source": peak_src,
-                         "algorithmic_bytes": "sizeof(f32)*(n + 2(n-w+1)) per launch"},
+                       "l2": "inputs (>= 128 MiB per GPU) and outputs larger than the 126 MB L2 "
+                             "(n_per_gpu >= 2^25 floats at N <= 8); no flush",
+                       "parallelism": (f"one array in {world} contiguous chunks (starts aligned to 256), (w_max-1) "
+                                       f"halo by NCCL send/recv on a comm stream, overlapped with the interior "
+                                       f"windows (maxmin_filter_1d_sharded)") if world > 1 else "single GPU"},
+            "hbm_gbs_step": sum(algo_bytes_1d(4, n_local, w) for w in windows) / (ms_max / args.steps / 1e3) / 1e9,
+            "roofline": roofline(per_w[str(dom)]["gbs"], ncu_traffic(args.config, dom), f"w={dom}",
+                                 "sizeof(f32)*(n + 2(n-w+1)) per launch, n = elements per GPU"),
             "per_window": per_w,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": sum(int(round(per_w[str(w)]["launches_per_step"])) for w in windows)
-            * args.steps,
+            "gpu_launches": launches * args.steps,
             "clocks": clk.summary(),
             "parity": parity,
         }
+        if world > 1:
+            line["halo_bytes_per_boundary"] = 4 * halo
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def spot_check(a, outs, windows, chunk, rank):
-    """Bounded oracle check of the bench outputs (windows fully inside the chunk)."""
+def spot_check(glob, c0, n_local, last, outs, windows):
+    """Bit-exact check of the bench outputs against the oracle (appendix listing) on
+    the global array: slices at the chunk start, middle and end (tile seams inside),
+    and -- for every rank but the last -- every window that reaches into the halo
+    (plus the 64 before them that the tail call recomputes)."""
     import numpy as np
 
     import oracle
 
     ok = True
     checked = 0
-    n = chunk.n_local
+    seam = 0
     for w in windows:
         ox, on = outs[w]
-        m_int = n - w + 1
-        for j0 in (0, 4096 - 7, m_int // 2 + 13, m_int - 4100):
-            j0 = max(0, min(j0, m_int - 1))
-            k = min(4100, m_int - j0)
-            ex, en, _ = oracle.appendix(a[j0: j0 + k + w - 1], w)
+        m = ox.shape[0]
+        ranges = [(0, 4100), (4096 - 7, 4100), (m // 2 + 13, 4100), (m - 4100, 4100)]
+        if not last:
+            ranges.append((n_local - w + 1 - 64, m))
+        for j0, k in ranges:
+            j0 = max(0, min(j0, m - 1))
+            k = min(k, m - j0)
+            g0 = c0 + j0
+            ex, en, _ = oracle.appendix(glob[g0: g0 + k + w - 1], w)
             gx = ox[j0: j0 + k].cpu().numpy()
             gn = on[j0: j0 + k].cpu().numpy()
-            ok &= np.array_equal(gx.view(np.uint32), ex.view(np.uint32))
-            ok &= np.array_equal(gn.view(np.uint32), en.view(np.uint32))
+            ok &= bool(np.array_equal(gx.view(np.uint32), ex.view(np.uint32))
+                       and np.array_equal(gn.view(np.uint32), en.view(np.uint32)))
             checked += 2 * k
-    return {"bit_exact": bool(ok), "outputs_checked": checked, "oracle": "oracle_appendix on slices"}
+            if not last and j0 + k == m:
+                seam += min(k, w - 1)
+    return {"bit_exact": bool(ok), "outputs_checked": checked, "seam_windows_checked": seam,
+            "oracle": "oracle_appendix on slices of the global array"}
 
 
 def run_e2e(args, host, n, windows, dev):
@@ -426,6 +571,45 @@ def run_e2e(args, host, n, windows, dev):
     d2h = 4 * outs
     return {"value": outs / dt, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": dt * 1e3, "steps": steps, "api": "maxmin_filter_1d_host (pinned host buffers)"}
+
+
+def run_e2e_sharded(args, step, host, buf, outs, n_local, windows, dev, world, n_total):
+    """N > 1: every step copies the rank's chunk from pinned host memory, runs the
+    sharded call (NCCL halo inside) and copies every output back to pinned host
+    memory; the time is the max over ranks (CUDA events, barrier on both sides)."""
+    import torch
+    import torch.distributed as dist
+
+    h_outs = {w: (torch.empty_like(outs[w][0], device="cpu").pin_memory(),
+                  torch.empty_like(outs[w][1], device="cpu").pin_memory()) for w in windows}
+    stream = torch.cuda.current_stream()
+
+    def e2e_step():
+        buf[:n_local].copy_(host[:n_local], non_blocking=True)
+        step()
+        for w in windows:
+            h_outs[w][0].copy_(outs[w][0], non_blocking=True)
+            h_outs[w][1].copy_(outs[w][1], non_blocking=True)
+
+    e2e_step()
+    steps = max(1, min(args.steps, 3))
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item()) / steps / 1e3
+    outs_n = sum(2 * (n_total - w + 1) for w in windows)
+    return {"value": outs_n / dt, "unit": UNIT, "h2d_bytes_per_step": 4 * n_local,
+            "d2h_bytes_per_step": sum(4 * (outs[w][0].numel() + outs[w][1].numel()) for w in windows),
+            "bytes_are": "rank 0's; every rank moves its own chunk and outputs",
+            "ms_per_step": dt * 1e3, "steps": steps,
+            "api": "H2D of the chunk, maxmin_filter_1d_sharded, D2H of the outputs (pinned host buffers)"}
 
 
 if __name__ == "__main__":

@@ -343,19 +343,16 @@ def run_extra(args, rank, world, local):
     achieved = nb / (ms_step / 1e3) / 1e9
     if rank == 0:
         cpu = None
-        if not args.no_cpu and world == 1 and sample is not None:
-            cpu = bench.cpu_baseline(cfg, np.ascontiguousarray(sample).reshape(-1) if cfg != "C3" else sample,
-                                     windows, None) if cfg == "C1" else _cpu_batched(sample, windows[0])
+        if not args.no_cpu and world == 1:
+            cpu = cpu_baseline_extra(cfg, host, windows[0])
         line = {
             "metric": bench.METRIC, "value": value, "unit": unit, "n_gpus": world, "steps": steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak" if cfg != "C1" else "replicas",
             "vs_baseline": None, "dtype": dtype, "data": "synthetic",
             "config": {"workload": name, "l2": l2,
                        "parallelism": f"item sharding, dp{world}" if world > 1 else "single GPU"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": bench.ncu_traffic(cfg, windows[0]),
-                         "traffic_unit": "dram bytes per launch of the dominant kernel (profiles/ncu_traffic.json)",
-                         "peak_source": peak_src},
+            "roofline": bench.roofline(achieved, bench.ncu_traffic(cfg, windows[0]), cfg,
+                                       "the config's algorithmic bytes per step (DESIGN.md section 7)"),
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": steps * {"N3": 3, "N2": 16}.get(cfg, 1), "clocks": clk,
             "parity": {"bit_exact": parity},
@@ -366,11 +363,78 @@ def run_extra(args, rank, world, local):
         dist.destroy_process_group()
 
 
-def _cpu_batched(sample, w):
+def _threads_timed(jobs, threads):
+    """Run the callables on `threads` host threads (ctypes calls release the GIL);
+    best of 2 wall times."""
+    import concurrent.futures as cf
+
+    best = None
+    for _ in range(2):
+        t0 = time.perf_counter()
+        if threads == 1:
+            for j in jobs:
+                j()
+        else:
+            with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+                list(ex.map(lambda j: j(), jobs))
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return best
+
+
+def cpu_baseline_extra(cfg, host, w):
+    """The oracle on a bounded sample of the config's own input, on 1 host thread and
+    on all of them (independent rows / row bands / series chunks per thread)."""
+    import numpy as np
+
     import oracle
 
-    t0 = time.perf_counter()
-    mx, mn = oracle.batched(sample, w)
-    dt = time.perf_counter() - t0
-    return {"value": 2 * mx.size / dt, "unit": bench.UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{sample.shape[0]} series x {sample.shape[1]}, oracle_batched (appendix per row), {dt:.2f} s"}
+    allt = oracle.host_threads()
+    h = host.numpy() if hasattr(host, "numpy") else host
+    if cfg == "C1":
+        return bench.cpu_baseline(cfg, np.ascontiguousarray(h), (w,))
+    if cfg in ("C3", "N2", "N4", "N3"):
+        rows = h[:4096]
+        k = rows.shape[0]
+        per = [(i * k // allt, (i + 1) * k // allt) for i in range(allt)]
+        if cfg == "N3":
+            import synth
+
+            q = synth.c3(rows=1, row0=synth.C3["batch"])[0]
+            job = lambda a, b: (lambda: oracle.keogh(rows[a:b], q, (w - 1) // 2))  # noqa: E731
+            outs, what, unit = k, "oracle.keogh (clipped envelope + bound per series)", "bounds/s"
+        elif cfg == "N4":
+            job = lambda a, b: (lambda: [oracle.morph(rows[i], w) for i in range(a, b)])  # noqa: E731
+            outs, what, unit = 2 * k * rows.shape[1], "oracle.morph per series", bench.UNIT
+        elif cfg == "N2":
+            def job(a, b):
+                return lambda: oracle.stream_pushes(rows[a:b], w, [256] * (rows.shape[1] // 256))
+            outs, what, unit = 2 * k * rows.shape[1], "oracle.Stream, 16 pushes of 256 per series", bench.UNIT
+        else:
+            job = lambda a, b: (lambda: oracle.batched(rows[a:b], w))  # noqa: E731
+            outs, what, unit = 2 * k * (rows.shape[1] - w + 1), "oracle.batched (appendix per row)", bench.UNIT
+        t1 = _threads_timed([job(0, k)], 1)
+        tn = _threads_timed([job(a, b) for a, b in per], allt)
+        sample = f"first {k} series of the bench input; {what}"
+    elif cfg == "C4":
+        img = h[0, :2048 + w - 1]
+        R = 2048
+        per = [(i * R // allt, (i + 1) * R // allt) for i in range(allt)]
+        job = lambda a, b: (lambda: oracle.separable_2d(img[a:b + w - 1], w, w))  # noqa: E731
+        outs, unit = 2 * R * (img.shape[1] - w + 1), bench.UNIT
+        t1 = _threads_timed([job(0, R)], 1)
+        tn = _threads_timed([job(a, b) for a, b in per], allt)
+        sample = f"first {R} output rows of image 0; oracle.separable_2d on row bands (w-1 rows of overlap)"
+    elif cfg == "N1":
+        a = np.ascontiguousarray(h[: 1 << 24])
+        m = a.shape[0] - w + 1
+        per = [(i * m // allt, (i + 1) * m // allt) for i in range(allt)]
+        job = lambda j0, j1: (lambda: oracle.arg_wedge(a[j0:j1 + w - 1], w))  # noqa: E731
+        outs, unit = 2 * m, bench.UNIT
+        t1 = _threads_timed([job(0, m)], 1)
+        tn = _threads_timed([job(j0, j1) for j0, j1 in per], allt)
+        sample = "first 2^24 elements; oracle.arg_wedge on contiguous window ranges"
+    else:
+        return None
+    return {"value": outs / tn, "unit": unit, "cores": allt, "kind": "oracle", "value_1thread": outs / t1,
+            "sample": sample + f", {allt} threads and 1 thread, best of 2 (oracle gcc -O2 build)"}

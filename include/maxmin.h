@@ -19,10 +19,14 @@
  *   scratch space is passed in through `workspace`.
  * - Lengths, counts, leading dimensions and strides are in ELEMENTS (int64).
  * - Work is enqueued asynchronously on `stream` (a cudaStream_t passed as
- *   void*; NULL = legacy default stream) of the current device.  Argument
- *   errors are detected synchronously: nothing is launched and a non-zero
- *   status is returned.  A launch failure returns MAXMIN_ERR_CUDA and
- *   maxmin_last_cuda_error() reports the cudaError_t.
+ *   void*; NULL = legacy default stream), which must belong to the device
+ *   that owns the call's data pointers.  All data pointers of one call must
+ *   be on one device (else MAXMIN_ERR_DEVICE); the library makes that device
+ *   current for the duration of the call and restores the caller's current
+ *   device before returning, on every path.  Argument errors are detected
+ *   synchronously: nothing is launched and a non-zero status is returned.  A
+ *   launch failure returns MAXMIN_ERR_CUDA and maxmin_last_cuda_error()
+ *   reports the cudaError_t.
  * - Alignment: data pointers must be 16-byte aligned and every leading
  *   dimension / stride times sizeof(element) must be a multiple of 16 bytes
  *   (else MAXMIN_ERR_ALIGNMENT).  Loads never touch bytes outside the 16-byte
@@ -70,7 +74,9 @@ typedef enum {
   MAXMIN_ERR_WORKSPACE = 8,         /* workspace NULL or smaller than required          */
   MAXMIN_ERR_CUDA = 9,              /* a CUDA runtime call failed                       */
   MAXMIN_ERR_UNSUPPORTED = 10,      /* valid request outside this build's limits        */
-  MAXMIN_ERR_MEMORY = 11            /* a data pointer is not device memory (device APIs) */
+  MAXMIN_ERR_MEMORY = 11,           /* a data pointer is not device memory (device APIs) */
+  MAXMIN_ERR_DEVICE = 12,           /* the data pointers of one call are on different devices */
+  MAXMIN_ERR_NCCL = 13              /* NCCL missing or an NCCL call failed (sharded call)  */
 } maxmin_status;
 
 /* Human-readable name of a status code (static storage). */
@@ -320,6 +326,51 @@ int maxmin_host_workspace_bytes(int dt, int64_t n, int64_t w, int64_t chunk,
 int maxmin_filter_1d_host(int dt, const void *in, int64_t n, int64_t w,
                           void *out_max, void *out_min, int64_t chunk,
                           void *dev_workspace, size_t workspace_bytes);
+
+/*
+ * One 1-D array split over `nranks` processes, one GPU each (
+ * the filter of PAPER.md:39-42 on the concatenation of the chunks).  Rank r
+ * owns the contiguous chunk [c_r, c_{r+1}) of the global array and emits every
+ * window that STARTS in it: n_local windows, or n_local-w+1 on the last rank
+ * (rank nranks-1).  The windows of the last w-1 starts need the first w-1
+ * elements of rank r+1's chunk -- the halo:
+ *   local      device buffer of n_local + halo elements (16-byte aligned):
+ *              [own chunk | halo slot].  The slot is overwritten.
+ *   halo       >= w-1 for every window; must not exceed the next rank's
+ *              n_local (not checkable here: the caller's partition).
+ *   windows    host array of nwin windows; out_max[k] / out_min[k] (host
+ *              arrays of device pointers; per window either may be NULL, not
+ *              both) receive the windows of windows[k]: n_local elements, or
+ *              n_local - windows[k] + 1 on the last rank, 16-byte aligned.
+ *   nccl_comm  an ncclComm_t whose size is nranks and whose rank is `rank`
+ *              (e.g. PyTorch ProcessGroupNCCL._comm_ptr()).  Exchange: one
+ *              ncclSend of the own first `halo` elements to rank-1 and one
+ *              ncclRecv of rank+1's into the slot, grouped, on comm_stream
+ *              (NULL = stream).  The windows inside the own chunk run on
+ *              `stream` while the message is in flight; the tail windows
+ *              (from the last 64-aligned start before n_local-w+1) wait for
+ *              the receive.  Every rank must make the call (NCCL point-to-
+ *              point semantics).  NCCL is loaded at run time (the libnccl.so.2
+ *              already in the process, else the system's); failure of either
+ *              -> MAXMIN_ERR_NCCL, maxmin_last_nccl_error() has ncclResult_t.
+ *              nccl_comm == NULL: the slot is taken as already filled by the
+ *              caller (its own transport, e.g. peer copies) and no exchange
+ *              happens.
+ *   workspace  device scratch of maxmin_sharded_workspace_bytes(...).
+ * Returns when everything is enqueued; `stream` is ordered after the whole
+ * call (including the receive).  The communicator's rank/size must match
+ * (else MAXMIN_ERR_SHAPE).
+ */
+int maxmin_sharded_workspace_bytes(int dt, int64_t n_local, int64_t halo,
+                                   const int64_t *windows, int nwin, size_t *bytes);
+int maxmin_filter_1d_sharded(int dt, void *local, int64_t n_local, int64_t halo,
+                             const int64_t *windows, int nwin, int rank, int nranks,
+                             void *nccl_comm, void *const *out_max, void *const *out_min,
+                             void *workspace, size_t workspace_bytes, void *stream,
+                             void *comm_stream);
+/* ncclResult_t of the last failing NCCL call of this library in the calling
+   thread (0 if none). */
+int maxmin_last_nccl_error(void);
 
 #ifdef __cplusplus
 }

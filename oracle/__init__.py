@@ -108,6 +108,78 @@ def _ptr(a: np.ndarray):
     return ctypes.c_void_p(a.ctypes.data)
 
 
+# ---------------------------------------------------------------- CPU baseline
+# The same C sources built with -O3 -march=native, used ONLY to time the oracle
+# as the CPU baseline ("O3 built with g++ -O3
+# -march=native", one thread and all host threads).  -march=native binds the
+# build to the host it runs on, so it is compiled there, on first use.
+_NATIVE_PATH = os.path.join(_HERE, "liboracle_native.so")
+_native = None
+NATIVE_FLAGS = ["-O3", "-march=native"]
+
+
+def build_native(force: bool = False) -> str:
+    src = [os.path.join(_HERE, "oracle.c"), os.path.join(_HERE, "oracle_body.inc"),
+           os.path.join(_HERE, "oracle.h")]
+    if not force and os.path.exists(_NATIVE_PATH):
+        if os.path.getmtime(_NATIVE_PATH) >= max(os.path.getmtime(s) for s in src):
+            return _NATIVE_PATH
+    tmp = _NATIVE_PATH + f".{os.getpid()}.tmp"
+    subprocess.check_call(["gcc", *NATIVE_FLAGS, "-std=c99", "-Wall", "-shared", "-fPIC", "-o", tmp, src[0], "-lm"])
+    os.replace(tmp, _NATIVE_PATH)
+    return _NATIVE_PATH
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def appendix_baseline(a, w: int, threads: int = 1, out_max=None, out_min=None):
+    """The appendix listing from the -O3 -march=native build,
+    on `threads` host threads: the m windows are cut into contiguous ranges, each
+    range filtered from its own input slice (the range plus w-1 elements of
+    overlap) by one sequential call.  ctypes releases the GIL during the calls,
+    so the threads run in parallel.  Returns (max, min)."""
+    global _native
+    if _native is None:
+        build_native()
+        _native = ctypes.CDLL(_NATIVE_PATH)
+    a = np.ascontiguousarray(a)
+    n = a.shape[0]
+    m = n - w + 1
+    if m <= 0:
+        raise OracleError(-2)
+    mx = np.empty(m, a.dtype) if out_max is None else out_max
+    mn = np.empty(m, a.dtype) if out_min is None else out_min
+    f = getattr(_native, f"oracle_appendix_{_SUFFIX[a.dtype]}")
+    f.restype = ctypes.c_int
+    sz = a.dtype.itemsize
+    threads = max(1, min(threads, m))
+    bounds = [m * k // threads for k in range(threads + 1)]
+
+    def run(k):
+        j0, j1 = bounds[k], bounds[k + 1]
+        if j1 <= j0:
+            return 0
+        st = _Stats()
+        return f(ctypes.c_void_p(a.ctypes.data + j0 * sz), ctypes.c_int64(j1 - j0 + w - 1), ctypes.c_int64(w),
+                 ctypes.c_void_p(mx.ctypes.data + j0 * sz), ctypes.c_void_p(mn.ctypes.data + j0 * sz),
+                 ctypes.byref(st))
+
+    if threads == 1:
+        _check(run(0))
+    else:
+        import concurrent.futures as cf
+
+        with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+            for rc in ex.map(run, range(threads)):
+                _check(rc)
+    return mx, mn
+
+
 def _fn(name: str, dtype):
     dt = np.dtype(dtype)
     if dt not in _SUFFIX:

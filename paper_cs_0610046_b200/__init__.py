@@ -22,7 +22,8 @@ __all__ = [
     "maxmin_filter_batched", "maxmin_filter_2d", "maxmin_filter_1d_host",
     "maxmin_host_workspace_bytes", "maxmin_argfilter_workspace_bytes", "maxmin_argfilter_batched",
     "maxmin_argfilter_1d", "maxmin_lb_keogh_batched", "maxmin_stream_state_bytes", "MaxMinStream", "maxmin_morph_batched",
-    "maxmin_morph_1d", "maxmin_morph_2d", "maxmin_filter_3d", "version",
+    "maxmin_morph_1d", "maxmin_morph_2d", "maxmin_filter_3d", "maxmin_sharded_workspace_bytes",
+    "maxmin_filter_1d_sharded", "version",
 ]
 
 _CODES = {
@@ -52,7 +53,7 @@ except AttributeError:  # pragma: no cover
 def _stream_ptr(stream, device=None) -> ctypes.c_void_p:
     if stream is None:
         if _raw_stream is not None:
-            idx = torch.cuda.current_device() if device is None else device.index
+            idx = torch.cuda.current_device() if device is None or device.index is None else device.index
             return ctypes.c_void_p(_raw_stream(idx))
         stream = torch.cuda.current_stream()
     return ctypes.c_void_p(stream.cuda_stream)
@@ -60,6 +61,37 @@ def _stream_ptr(stream, device=None) -> ctypes.c_void_p:
 
 def _ptr(t) -> ctypes.c_void_p:
     return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _check_out(name: str, t, x: torch.Tensor, shape) -> None:
+    """A caller-supplied output: the input's dtype and device, at least `shape`
+    (leading dims exact, last dim >= shape[-1]) and unit stride along the last
+    dim -- the C ABI cannot see buffer sizes, so an undersized or mistyped output
+    would be written past its end."""
+    if t is None:
+        return
+    if t.dtype != x.dtype or t.device != x.device:
+        raise ValueError(f"{name}: dtype/device {t.dtype}/{t.device} differ from the input's {x.dtype}/{x.device}")
+    if t.dim() != len(shape) or tuple(t.shape[:-1]) != tuple(shape[:-1]) or t.shape[-1] < shape[-1]:
+        raise ValueError(f"{name}: shape {tuple(t.shape)} does not hold {tuple(shape)}")
+    if shape[-1] > 0 and t.stride(-1) != 1:
+        raise ValueError(f"{name}: the last dimension must be contiguous")
+
+
+def _pair_strides(name: str, a, b, dims: int) -> None:
+    """Both outputs share one row (and image) stride: the C ABI takes one pitch."""
+    if a is not None and b is not None and tuple(a.stride()[:dims]) != tuple(b.stride()[:dims]):
+        raise ValueError(f"{name}: out_max and out_min must have the same strides")
+
+
+def _alloc_out(ref, shape, dtype, device):
+    """A fresh output of `shape`: with the strides of `ref` (the caller's other
+    output) when given, so both share one pitch; else rows padded to 16 bytes."""
+    if ref is not None:
+        return torch.empty_strided(tuple(shape), tuple(ref.stride()), dtype=dtype, device=device)
+    vec = max(16 // torch.empty((), dtype=dtype).element_size(), 1)
+    pad = (shape[-1] + vec - 1) // vec * vec
+    return torch.empty(*shape[:-1], pad, dtype=dtype, device=device)[..., : shape[-1]]
 
 
 @functools.lru_cache(maxsize=256)
@@ -89,6 +121,8 @@ def maxmin_filter_1d(x: torch.Tensor, w: int, out_max=None, out_min=None, *, wan
         raise ValueError("maxmin_filter_1d: x must be a contiguous 1-D CUDA tensor")
     n = x.shape[0]
     m = max(n - w + 1, 0)
+    _check_out("out_max", out_max, x, (m,))
+    _check_out("out_min", out_min, x, (m,))
     if want_max and out_max is None and m > 0:
         out_max = torch.empty(m, dtype=x.dtype, device=x.device)
     if want_min and out_min is None and m > 0:
@@ -107,13 +141,15 @@ def maxmin_filter_batched(x: torch.Tensor, w: int, n: int | None = None, out_max
     batch, ncols = x.shape
     n = ncols if n is None else n
     m = max(n - w + 1, 0)
-    # rows of the outputs are padded to 16 bytes (the C ABI's alignment rule)
-    vec = max(16 // x.element_size(), 1)
-    m_pad = (m + vec - 1) // vec * vec
+    _check_out("out_max", out_max, x, (batch, m))
+    _check_out("out_min", out_min, x, (batch, m))
+    _pair_strides("maxmin_filter_batched", out_max, out_min, 1)
+    # rows of fresh outputs are padded to 16 bytes (the C ABI's alignment rule),
+    # or take the pitch of the output the caller supplied
     if want_max and out_max is None and m > 0:
-        out_max = torch.empty(batch, m_pad, dtype=x.dtype, device=x.device)[:, :m]
+        out_max = _alloc_out(out_min, (batch, m), x.dtype, x.device)
     if want_min and out_min is None and m > 0:
-        out_min = torch.empty(batch, m_pad, dtype=x.dtype, device=x.device)[:, :m]
+        out_min = _alloc_out(out_max, (batch, m), x.dtype, x.device)
     out_ld = (out_max if out_max is not None else out_min).stride(0) if m > 0 else 1
     ws, wsb = _workspace(x.dtype, batch, n, w, x.device, workspace) if 1 <= w <= n else (None, 0)
     _lib.check(_lib.lib().maxmin_filter_batched(dtype_code(x.dtype), _ptr(x), batch, n, x.stride(0), w,
@@ -146,15 +182,17 @@ def maxmin_filter_2d(x: torch.Tensor, w_row: int, w_col: int, cols: int | None =
     batch, rows, ld = xx.shape
     cols = ld if cols is None else cols
     R, C = rows - w_col + 1, cols - w_row + 1
-    vec = max(16 // x.element_size(), 1)
-    C_pad = (C + vec - 1) // vec * vec
+    if squeeze:  # [rows, ld] input: outputs may be given as [R, C]
+        out_max = out_max[None] if out_max is not None and out_max.dim() == 2 else out_max
+        out_min = out_min[None] if out_min is not None and out_min.dim() == 2 else out_min
+    _check_out("out_max", out_max, x, (batch, max(R, 0), max(C, 0)))
+    _check_out("out_min", out_min, x, (batch, max(R, 0), max(C, 0)))
+    _pair_strides("maxmin_filter_2d", out_max, out_min, 2)
     if want_max and out_max is None and R > 0 and C > 0:
-        out_max = torch.empty(batch, R, C_pad, dtype=x.dtype, device=x.device)[:, :, :C]
+        out_max = _alloc_out(out_min, (batch, R, C), x.dtype, x.device)
     if want_min and out_min is None and R > 0 and C > 0:
-        out_min = torch.empty(batch, R, C_pad, dtype=x.dtype, device=x.device)[:, :, :C]
+        out_min = _alloc_out(out_max, (batch, R, C), x.dtype, x.device)
     om = out_max if out_max is not None else out_min
-    if om is not None and om.dim() == 2:
-        om = om[None]
     out_ld = om.stride(1) if om is not None else 1
     out_bs = om.stride(0) if om is not None else 1
     need = _workspace_2d(dtype_code(x.dtype), batch, rows, cols, w_row, w_col) if R > 0 and C > 0 else 0
@@ -199,7 +237,7 @@ def maxmin_argfilter_batched(x: torch.Tensor, w: int, n: int | None = None, *, w
     _lib.check(_lib.lib().maxmin_argfilter_batched(
         dtype_code(x.dtype), _ptr(x), batch, n, x.stride(0), w, _ptr(out_max), _ptr(out_min),
         _ptr(arg_max), _ptr(arg_min), out_ld, _ptr(workspace), workspace.numel() * workspace.element_size(),
-        _stream_ptr(stream)))
+        _stream_ptr(stream, x.device)))
     return out_max, out_min, arg_max, arg_min
 
 
@@ -223,7 +261,7 @@ def maxmin_lb_keogh_batched(cand: torch.Tensor, query: torch.Tensor, r: int, n: 
         raise ValueError("maxmin_lb_keogh_batched: query must be a contiguous 1-D CUDA tensor of n samples")
     lb = torch.empty(batch, dtype=torch.float64, device=cand.device) if out is None else out
     _lib.check(_lib.lib().maxmin_lb_keogh_batched(dtype_code(cand.dtype), _ptr(cand), batch, n, cand.stride(0),
-                                                  _ptr(query), r, _ptr(lb), _stream_ptr(stream)))
+                                                  _ptr(query), r, _ptr(lb), _stream_ptr(stream, cand.device)))
     return lb
 
 
@@ -249,7 +287,7 @@ class MaxMinStream:
         self.state = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)
         self._st = _lib.Stream()
         _lib.check(_lib.lib().maxmin_stream_init(ctypes.byref(self._st), dtype_code(dtype), streams, w, max_chunk,
-                                                 _ptr(self.state), nbytes, _stream_ptr(stream)))
+                                                 _ptr(self.state), nbytes, _stream_ptr(stream, self.state.device)))
 
     @property
     def seen(self) -> int:
@@ -276,16 +314,19 @@ class MaxMinStream:
         c = chunk.shape[1]
         vec = max(16 // chunk.element_size(), 1)
         c_pad = max((c + vec - 1) // vec * vec, vec)
+        _check_out("out_max", out_max, chunk, (self.streams, c))
+        _check_out("out_min", out_min, chunk, (self.streams, c))
+        _pair_strides("MaxMinStream.push", out_max, out_min, 1)
         if want_max and out_max is None:
-            out_max = torch.empty(self.streams, c_pad, dtype=self.dtype, device=chunk.device)[:, :c]
+            out_max = _alloc_out(out_min, (self.streams, c), self.dtype, chunk.device)
         if want_min and out_min is None:
-            out_min = torch.empty(self.streams, c_pad, dtype=self.dtype, device=chunk.device)[:, :c]
+            out_min = _alloc_out(out_max, (self.streams, c), self.dtype, chunk.device)
         om = out_max if out_max is not None else out_min
         out_ld = om.stride(0) if om is not None else c_pad
         fv = ctypes.c_int64(0)
         _lib.check(_lib.lib().maxmin_stream_push(
             ctypes.byref(self._st), _ptr(chunk), c, chunk.stride(0), _ptr(out_max), _ptr(out_min), out_ld,
-            ctypes.byref(fv), _stream_ptr(stream)))
+            ctypes.byref(fv), _stream_ptr(stream, chunk.device)))
         return out_max, out_min, int(fv.value)
 
 
@@ -297,16 +338,17 @@ def maxmin_morph_batched(x: torch.Tensor, w: int, n: int | None = None, out_open
         raise ValueError("maxmin_morph_batched: x must be a row-major 2-D CUDA tensor")
     batch, ncols = x.shape
     n = ncols if n is None else n
-    vec = max(16 // x.element_size(), 1)
-    n_pad = (n + vec - 1) // vec * vec
+    _check_out("out_open", out_open, x, (batch, n))
+    _check_out("out_close", out_close, x, (batch, n))
+    _pair_strides("maxmin_morph_batched", out_open, out_close, 1)
     if want_open and out_open is None:
-        out_open = torch.empty(batch, n_pad, dtype=x.dtype, device=x.device)[:, :n]
+        out_open = _alloc_out(out_close, (batch, n), x.dtype, x.device)
     if want_close and out_close is None:
-        out_close = torch.empty(batch, n_pad, dtype=x.dtype, device=x.device)[:, :n]
+        out_close = _alloc_out(out_open, (batch, n), x.dtype, x.device)
     o = out_open if out_open is not None else out_close
     _lib.check(_lib.lib().maxmin_morph_batched(dtype_code(x.dtype), _ptr(x), batch, n, x.stride(0), w,
                                                _ptr(out_open), _ptr(out_close), o.stride(0) if o is not None else n,
-                                               _stream_ptr(stream)))
+                                               _stream_ptr(stream, x.device)))
     return out_open, out_close
 
 
@@ -328,13 +370,17 @@ def maxmin_morph_2d(x: torch.Tensor, w_row: int, w_col: int, cols: int | None = 
         raise ValueError("maxmin_morph_2d: x must be a row-major [batch, rows, ld] CUDA tensor")
     batch, rows, ld = xx.shape
     cols = ld if cols is None else cols
+    if squeeze:
+        out_open = out_open[None] if out_open is not None and out_open.dim() == 2 else out_open
+        out_close = out_close[None] if out_close is not None and out_close.dim() == 2 else out_close
+    _check_out("out_open", out_open, x, (batch, rows, cols))
+    _check_out("out_close", out_close, x, (batch, rows, cols))
+    _pair_strides("maxmin_morph_2d", out_open, out_close, 2)
     if want_open and out_open is None:
-        out_open = torch.empty(batch, rows, cols, dtype=x.dtype, device=x.device)
+        out_open = _alloc_out(out_close, (batch, rows, cols), x.dtype, x.device)
     if want_close and out_close is None:
-        out_close = torch.empty(batch, rows, cols, dtype=x.dtype, device=x.device)
+        out_close = _alloc_out(out_open, (batch, rows, cols), x.dtype, x.device)
     o = out_open if out_open is not None else out_close
-    if o is not None and o.dim() == 2:
-        o = o[None]
     need = ctypes.c_size_t(0)
     _lib.check(_lib.lib().maxmin_morph_2d_workspace_bytes(dtype_code(x.dtype), batch, rows, cols, w_row, w_col,
                                                           ctypes.byref(need)))
@@ -342,7 +388,7 @@ def maxmin_morph_2d(x: torch.Tensor, w_row: int, w_col: int, cols: int | None = 
         workspace = torch.empty(max(need.value, 16), dtype=torch.uint8, device=x.device)
     _lib.check(_lib.lib().maxmin_morph_2d(
         dtype_code(x.dtype), _ptr(xx), batch, rows, cols, xx.stride(1), xx.stride(0), w_row, w_col, _ptr(out_open),
-        _ptr(out_close), o.stride(1), o.stride(0), _ptr(workspace), workspace.numel(), _stream_ptr(stream)))
+        _ptr(out_close), o.stride(1), o.stride(0), _ptr(workspace), workspace.numel(), _stream_ptr(stream, x.device)))
     if squeeze:
         out_open = out_open[0] if out_open is not None and out_open.dim() == 3 else out_open
         out_close = out_close[0] if out_close is not None and out_close.dim() == 3 else out_close
@@ -358,10 +404,13 @@ def maxmin_filter_3d(x: torch.Tensor, w_x: int, w_y: int, w_z: int, cols: int | 
     depth, rows, ld = x.shape
     cols = ld if cols is None else cols
     D, R, C = depth - w_z + 1, rows - w_y + 1, cols - w_x + 1
+    _check_out("out_max", out_max, x, (max(D, 0), max(R, 0), max(C, 0)))
+    _check_out("out_min", out_min, x, (max(D, 0), max(R, 0), max(C, 0)))
+    _pair_strides("maxmin_filter_3d", out_max, out_min, 2)
     if want_max and out_max is None and min(D, R, C) > 0:
-        out_max = torch.empty(D, R, C, dtype=x.dtype, device=x.device)
+        out_max = _alloc_out(out_min, (D, R, C), x.dtype, x.device)
     if want_min and out_min is None and min(D, R, C) > 0:
-        out_min = torch.empty(D, R, C, dtype=x.dtype, device=x.device)
+        out_min = _alloc_out(out_max, (D, R, C), x.dtype, x.device)
     o = out_max if out_max is not None else out_min
     need = ctypes.c_size_t(0)
     _lib.check(_lib.lib().maxmin_filter_3d_workspace_bytes(dtype_code(x.dtype), depth, rows, cols, x.stride(1), w_x,
@@ -371,7 +420,7 @@ def maxmin_filter_3d(x: torch.Tensor, w_x: int, w_y: int, w_z: int, cols: int | 
     _lib.check(_lib.lib().maxmin_filter_3d(
         dtype_code(x.dtype), _ptr(x), depth, rows, cols, x.stride(1), x.stride(0), w_x, w_y, w_z, _ptr(out_max),
         _ptr(out_min), o.stride(1) if o is not None else C, o.stride(0) if o is not None else R * C, _ptr(workspace),
-        workspace.numel(), _stream_ptr(stream)))
+        workspace.numel(), _stream_ptr(stream, x.device)))
     return out_max, out_min
 
 
@@ -386,7 +435,59 @@ def maxmin_filter_1d_host(x: torch.Tensor, w: int, out_max: torch.Tensor, out_mi
     """End-to-end call on HOST (preferably pinned) tensors: H2D, filter, D2H inside."""
     if x.is_cuda or out_max.is_cuda or out_min.is_cuda:
         raise ValueError("maxmin_filter_1d_host: x/out_max/out_min must be host tensors")
+    if x.dim() != 1 or not x.is_contiguous():
+        raise ValueError("maxmin_filter_1d_host: x must be a contiguous 1-D host tensor")
+    m = max(x.shape[0] - w + 1, 0)
+    for name, t in (("out_max", out_max), ("out_min", out_min)):
+        if t.dtype != x.dtype or t.dim() != 1 or not t.is_contiguous() or t.shape[0] < m:
+            raise ValueError(f"maxmin_filter_1d_host: {name} must be a contiguous {x.dtype} host tensor "
+                             f"of at least n-w+1 = {m} elements")
+    if not dev_workspace.is_cuda:
+        raise ValueError("maxmin_filter_1d_host: dev_workspace must be a CUDA tensor")
+    need = maxmin_host_workspace_bytes(x.dtype, x.shape[0], w, chunk) if 1 <= w <= x.shape[0] else 0
+    if dev_workspace.numel() * dev_workspace.element_size() < need:
+        raise ValueError(f"maxmin_filter_1d_host: dev_workspace holds fewer than {need} bytes")
     _lib.check(_lib.lib().maxmin_filter_1d_host(dtype_code(x.dtype), _ptr(x), x.shape[0], w,
                                                 _ptr(out_max), _ptr(out_min), chunk,
                                                 _ptr(dev_workspace),
                                                 dev_workspace.numel() * dev_workspace.element_size()))
+
+
+def maxmin_sharded_workspace_bytes(dtype, n_local: int, halo: int, windows) -> int:
+    ws = (ctypes.c_int64 * len(windows))(*windows)
+    out = ctypes.c_size_t(0)
+    _lib.check(_lib.lib().maxmin_sharded_workspace_bytes(dtype_code(dtype), n_local, halo, ws, len(windows),
+                                                         ctypes.byref(out)))
+    return int(out.value)
+
+
+def maxmin_filter_1d_sharded(local: torch.Tensor, n_local: int, halo: int, windows, out_max, out_min, rank: int,
+                             nranks: int, nccl_comm=None, *, workspace=None, stream=None, comm_stream=None):
+    """One array split over ranks (include/maxmin.h maxmin_filter_1d_sharded).
+
+    local: 1-D CUDA tensor [own chunk (n_local) | halo slot] (>= n_local + halo elements).
+    windows: the windows; out_max / out_min: one CUDA tensor (or None) per window,
+    n_local elements (n_local - w + 1 on the last rank).  nccl_comm: the ncclComm_t
+    as an int (shard.nccl_comm_ptr), or None when the caller already filled the halo
+    slot.  Enqueued on `stream` (NCCL on `comm_stream`); returns immediately."""
+    if local.dim() != 1 or not local.is_cuda or not local.is_contiguous() or local.shape[0] < n_local + halo:
+        raise ValueError("maxmin_filter_1d_sharded: local must be a contiguous 1-D CUDA tensor of n_local + halo")
+    windows = [int(w) for w in windows]
+    last = rank == nranks - 1
+    for name, outs in (("out_max", out_max), ("out_min", out_min)):
+        if len(outs) != len(windows):
+            raise ValueError(f"maxmin_filter_1d_sharded: {name} needs one entry per window")
+        for w, t in zip(windows, outs):
+            _check_out(f"{name}[w={w}]", t, local, (n_local - w + 1 if last else n_local,))
+    need = maxmin_sharded_workspace_bytes(local.dtype, n_local, halo, windows)
+    if workspace is None and need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=local.device)
+    wsb = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    arr = ctypes.c_int64 * len(windows)
+    vps = ctypes.c_void_p * len(windows)
+    cs = None if comm_stream is None else ctypes.c_void_p(comm_stream.cuda_stream)
+    _lib.check(_lib.lib().maxmin_filter_1d_sharded(
+        dtype_code(local.dtype), _ptr(local), n_local, halo, arr(*windows), len(windows), rank, nranks,
+        ctypes.c_void_p(nccl_comm or 0), vps(*[t.data_ptr() if t is not None else 0 for t in out_max]),
+        vps(*[t.data_ptr() if t is not None else 0 for t in out_min]), _ptr(workspace), wsb,
+        _stream_ptr(stream, local.device), cs))

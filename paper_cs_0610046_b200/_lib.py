@@ -20,17 +20,21 @@ STATUS = {
     4: "window larger than input", 5: "bad shape", 6: "misaligned pointer or leading dimension",
     7: "output overlaps input or the other output", 8: "workspace missing or too small",
     9: "CUDA error", 10: "unsupported by this build", 11: "pointer is not device memory",
+    12: "data pointers on different devices", 13: "NCCL error",
 }
 
 
 class MaxMinError(RuntimeError):
-    def __init__(self, status: int, cuda_error: int = 0):
+    def __init__(self, status: int, cuda_error: int = 0, nccl_error: int = 0):
         msg = f"maxmin status {status}: {STATUS.get(status, 'unknown')}"
         if status == 9:
             msg += f" (cudaError {cuda_error})"
+        if status == 13:
+            msg += f" (ncclResult {nccl_error})"
         super().__init__(msg)
         self.status = status
         self.cuda_error = cuda_error
+        self.nccl_error = nccl_error
 
 
 _lib = None
@@ -80,6 +84,12 @@ SIGNATURES = {
                                         _i64, _i64, _vp, _sz, _vp]),
     "maxmin_host_workspace_bytes": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _i64, ctypes.POINTER(_sz)]),
     "maxmin_filter_1d_host": (ctypes.c_int, [ctypes.c_int, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _sz]),
+    "maxmin_sharded_workspace_bytes": (ctypes.c_int, [ctypes.c_int, _i64, _i64, ctypes.POINTER(_i64), ctypes.c_int,
+                                                      ctypes.POINTER(_sz)]),
+    "maxmin_filter_1d_sharded": (ctypes.c_int, [ctypes.c_int, _vp, _i64, _i64, ctypes.POINTER(_i64), ctypes.c_int,
+                                                ctypes.c_int, ctypes.c_int, _vp, ctypes.POINTER(_vp),
+                                                ctypes.POINTER(_vp), _vp, _sz, _vp, _vp]),
+    "maxmin_last_nccl_error": (ctypes.c_int, []),
 }
 
 
@@ -101,4 +111,5 @@ def lib():
 
 def check(status: int) -> None:
     if status != 0:
-        raise MaxMinError(status, lib().maxmin_last_cuda_error())
+        L = lib()
+        raise MaxMinError(status, L.maxmin_last_cuda_error(), L.maxmin_last_nccl_error() if status == 13 else 0)

@@ -25,6 +25,13 @@ static int launch_byte(const k2b::Args &a, const CUtensorMap &map, cudaStream_t 
   return note_cuda(cudaGetLastError());
 }
 
+bool k2b_supports(int64_t w) {  // the square windows compiled into dispatch_square below
+  switch (w) {
+    case 2: case 3: case 4: case 5: case 7: case 9: case 11: case 13: case 15: case 16: case 17: return true;
+    default: return false;
+  }
+}
+
 template <bool SG>
 static int dispatch_square(const k2b::Args &a, const CUtensorMap &m, int w, cudaStream_t s) {
   switch (w) {
@@ -46,7 +53,7 @@ static int dispatch_square(const k2b::Args &a, const CUtensorMap &m, int w, cuda
 int launch_2d_byte(bool is_signed, const void *in, int64_t batch, int64_t rows, int64_t cols,
                    int64_t in_ld, int64_t in_bstride, int64_t w_row, int64_t w_col, void *out_max,
                    void *out_min, int64_t out_ld, int64_t out_bstride, cudaStream_t s) {
-  if (w_row != w_col || w_row > k2b::MAXW) return kErrUnsupported;
+  if (w_row != w_col || w_row > k2b::MAXW || !k2b_supports(w_row)) return kErrUnsupported;
   auto al = [](const void *p, uintptr_t m) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) % m) == 0; };
   if (!al(in, 16) || in_ld % 16 || (batch > 1 && in_bstride % 16)) return kErrUnsupported;
   if (!al(out_max, 4) || !al(out_min, 4) || out_ld % 4 || (batch > 1 && out_bstride % 4))

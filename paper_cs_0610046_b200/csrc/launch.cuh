@@ -26,6 +26,8 @@ int sm_count();                // SMs of the current device (cached)
 int launch_2d_byte(bool is_signed, const void *in, int64_t batch, int64_t rows, int64_t cols,
                    int64_t in_ld, int64_t in_bstride, int64_t w_row, int64_t w_col, void *out_max,
                    void *out_min, int64_t out_ld, int64_t out_bstride, cudaStream_t s);
+// square windows the packed 1-byte kernel is compiled for (k2d_byte.cu)
+bool k2b_supports(int64_t w);
 // LB_Keogh fused with the envelope (keogh.cu): float rows
 int launch_keogh(const float *c, int64_t batch, int64_t n, int64_t ld, const float *q, int64_t r, double *lb,
                  cudaStream_t s);

@@ -10,6 +10,7 @@
 #include "../../include/maxmin.h"
 #include "launch.cuh"
 
+#include <initializer_list>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -246,25 +247,50 @@ int validate_batched(int dt, const void *in, int64_t batch, int64_t n, int64_t i
   return MAXMIN_OK;
 }
 
-// Make the device that owns `p` current for this library's runtime (the
-// caller's framework may have another device current, e.g. one rank per GPU).
-int ensure_device(const void *p) {
-  cudaPointerAttributes a;
-  cudaError_t e = cudaPointerGetAttributes(&a, p);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return mm::note_cuda(e);
+// Binds the calling thread to the device that owns every data pointer of one
+// call for the duration of the call, and restores the caller's device on every
+// exit path (the library links cudart statically, so a switch would otherwise
+// leak into the caller's framework).  Pointers on different devices are an
+// error, not a silent pick of the last one.
+class DeviceScope {
+ public:
+  DeviceScope() = default;
+  DeviceScope(const DeviceScope &) = delete;
+  DeviceScope &operator=(const DeviceScope &) = delete;
+  ~DeviceScope() {
+    if (prev_ >= 0) cudaSetDevice(prev_);
   }
-  if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) return MAXMIN_ERR_MEMORY;
-  int cur = -1;
-  e = cudaGetDevice(&cur);
-  if (e != cudaSuccess) return mm::note_cuda(e);
-  if (cur != a.device) {
-    e = cudaSetDevice(a.device);
+  int bind(std::initializer_list<const void *> ptrs) {
+    int dev = -1;
+    for (const void *p : ptrs) {
+      if (!p) continue;
+      cudaPointerAttributes a;
+      cudaError_t e = cudaPointerGetAttributes(&a, p);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        return mm::note_cuda(e);
+      }
+      if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) return MAXMIN_ERR_MEMORY;
+      if (dev < 0)
+        dev = a.device;
+      else if (a.device != dev)
+        return MAXMIN_ERR_DEVICE;
+    }
+    if (dev < 0) return MAXMIN_OK;
+    int cur = -1;
+    cudaError_t e = cudaGetDevice(&cur);
     if (e != cudaSuccess) return mm::note_cuda(e);
+    if (cur != dev) {
+      e = cudaSetDevice(dev);
+      if (e != cudaSuccess) return mm::note_cuda(e);
+      prev_ = cur;
+    }
+    return MAXMIN_OK;
   }
-  return MAXMIN_OK;
-}
+
+ private:
+  int prev_ = -1;
+};
 
 }  // namespace
 
@@ -284,6 +310,8 @@ const char *maxmin_status_str(int status) {
     case MAXMIN_ERR_CUDA: return "CUDA error";
     case MAXMIN_ERR_UNSUPPORTED: return "unsupported by this build";
     case MAXMIN_ERR_MEMORY: return "pointer is not device memory";
+    case MAXMIN_ERR_DEVICE: return "data pointers on different devices";
+    case MAXMIN_ERR_NCCL: return "NCCL error";
     default: return "unknown status";
   }
 }
@@ -334,10 +362,8 @@ int maxmin_filter_batched(int dt, const void *in, int64_t batch, int64_t n, int6
     if (overlap(workspace, need, in, ib)) return MAXMIN_ERR_ALIAS;
   }
   if (batch == 0) return MAXMIN_OK;
-  if ((rc = ensure_device(in)) != MAXMIN_OK) return rc;
-  if (out_max && (rc = ensure_device(out_max)) != MAXMIN_OK) return rc;
-  if (out_min && (rc = ensure_device(out_min)) != MAXMIN_OK) return rc;
-  if (need > 0 && (rc = ensure_device(workspace)) != MAXMIN_OK) return rc;
+  DeviceScope dev;
+  if ((rc = dev.bind({in, out_max, out_min, (need > 0) ? workspace : nullptr})) != MAXMIN_OK) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   MM_DISPATCH(dt, return mm::launch_1d<T>(in, batch, n, in_ld, w, out_max, out_min, out_ld,
                                           workspace, workspace_bytes, s))
@@ -367,9 +393,8 @@ int maxmin_lb_keogh_batched(int dt, const void *cand, int64_t batch, int64_t n, 
   if (overlap(cand, cb, lb, (size_t)batch * 8) || overlap(query, (size_t)n * 4, lb, (size_t)batch * 8))
     return MAXMIN_ERR_ALIAS;
   int rc;
-  if ((rc = ensure_device(cand)) != MAXMIN_OK) return rc;
-  if ((rc = ensure_device(query)) != MAXMIN_OK) return rc;
-  if ((rc = ensure_device(lb)) != MAXMIN_OK) return rc;
+  DeviceScope dev;
+  if ((rc = dev.bind({cand, query, lb})) != MAXMIN_OK) return rc;
   return mm::launch_keogh(static_cast<const float *>(cand), batch, n, ld, static_cast<const float *>(query), r,
                           lb, static_cast<cudaStream_t>(stream));
 }
@@ -423,10 +448,8 @@ int maxmin_argfilter_batched(int dt, const void *in, int64_t batch, int64_t n, i
       if (outs[k] && overlap(outs[i], obytes[i], outs[k], obytes[k])) return MAXMIN_ERR_ALIAS;
   }
   if (workspace && overlap(workspace, need, in, ib)) return MAXMIN_ERR_ALIAS;
-  if ((rc = ensure_device(in)) != MAXMIN_OK) return rc;
-  for (int i = 0; i < 4; ++i)
-    if (outs[i] && (rc = ensure_device(outs[i])) != MAXMIN_OK) return rc;
-  if (workspace && (rc = ensure_device(workspace)) != MAXMIN_OK) return rc;
+  DeviceScope dev;
+  if ((rc = dev.bind({in, outs[0], outs[1], outs[2], outs[3], workspace})) != MAXMIN_OK) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   switch (dt) {
     case MAXMIN_U8: return mm::launch_argfilter<uint8_t>(in, batch, n, in_ld, w, out_max, out_min, arg_max, arg_min, out_ld, workspace, workspace_bytes, s);
@@ -479,9 +502,8 @@ int maxmin_filter_2d(int dt, const void *in, int64_t batch, int64_t rows, int64_
   int rc = validate_2d(dt, in, batch, rows, cols, in_ld, in_bstride, w_row, w_col, out_max, out_min, out_ld,
                        out_bstride, &ib, &ob);
   if (rc != MAXMIN_OK || batch == 0) return rc;
-  if ((rc = ensure_device(in)) != MAXMIN_OK) return rc;
-  if (out_max && (rc = ensure_device(out_max)) != MAXMIN_OK) return rc;
-  if (out_min && (rc = ensure_device(out_min)) != MAXMIN_OK) return rc;
+  DeviceScope dev;
+  if ((rc = dev.bind({in, out_max, out_min})) != MAXMIN_OK) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   MM_DISPATCH(dt, return mm::launch_2d<T>(in, batch, rows, cols, in_ld, in_bstride, w_row, w_col,
                                           out_max, out_min, out_ld, out_bstride, s))
@@ -500,7 +522,7 @@ int maxmin_filter_2d_workspace_bytes(int dt, int64_t batch, int64_t rows, int64_
   if (!extent(batch > 0 ? batch : 1, rows * (cols + 16), rows * (cols + 16), sz, &t)) return MAXMIN_ERR_SHAPE;
   // 1-byte pixels in the packed kernel's domain need no scratch (its alignment
   // rules aside: an unaligned call falls back to the fused generic kernel)
-  if (sz == 1 && w_row == w_col && w_row <= 17) return MAXMIN_OK;
+  if (sz == 1 && w_row == w_col && mm::k2b_supports(w_row)) return MAXMIN_OK;
   MM_DISPATCH(dt, { *bytes = mm::sep2d_workspace<T>(batch, rows, cols, w_row, w_col); return MAXMIN_OK; })
 }
 
@@ -520,10 +542,8 @@ int maxmin_filter_2d_ws(int dt, const void *in, int64_t batch, int64_t rows, int
         (out_min && overlap(workspace, wsb, out_min, ob)))
       return MAXMIN_ERR_ALIAS;
   }
-  if ((rc = ensure_device(in)) != MAXMIN_OK) return rc;
-  if (out_max && (rc = ensure_device(out_max)) != MAXMIN_OK) return rc;
-  if (out_min && (rc = ensure_device(out_min)) != MAXMIN_OK) return rc;
-  if (workspace && wsb && (rc = ensure_device(workspace)) != MAXMIN_OK) return rc;
+  DeviceScope dev;
+  if ((rc = dev.bind({in, out_max, out_min, (workspace && wsb) ? workspace : nullptr})) != MAXMIN_OK) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // the fused packed-byte kernel, else the separable streaming passes (when the
   // workspace suffices), else the fused generic kernel
@@ -585,7 +605,8 @@ int maxmin_stream_init(maxmin_stream *st, int dt, int64_t streams, int64_t w, in
   st->state = state;
   st->state_bytes = state_bytes;
   if (streams == 0) return MAXMIN_OK;
-  if ((rc = ensure_device(state)) != MAXMIN_OK) return rc;
+  DeviceScope dev;
+  if ((rc = dev.bind({state})) != MAXMIN_OK) return rc;
   return mm::note_cuda(cudaMemsetAsync(state, 0, L.fused ? 2 * L.hist_bytes : L.hist_bytes,
                                        static_cast<cudaStream_t>(stream)));
 }
@@ -618,10 +639,8 @@ int maxmin_stream_push(maxmin_stream *st, const void *chunk, int64_t c, int64_t 
     for (int k = i + 1; k < 4; ++k)
       if (regions[i] && regions[k] && overlap(regions[i], rbytes[i], regions[k], rbytes[k])) return MAXMIN_ERR_ALIAS;
   int rc;
-  if ((rc = ensure_device(st->state)) != MAXMIN_OK) return rc;
-  if ((rc = ensure_device(chunk)) != MAXMIN_OK) return rc;
-  if (out_max && (rc = ensure_device(out_max)) != MAXMIN_OK) return rc;
-  if (out_min && (rc = ensure_device(out_min)) != MAXMIN_OK) return rc;
+  DeviceScope dev;
+  if ((rc = dev.bind({st->state, chunk, out_max, out_min})) != MAXMIN_OK) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   MM_DISPATCH(dt, {
     rc = mm::launch_stream_push<T>(st->state, L, st->streams, st->w, st->phase, static_cast<const T *>(chunk), c,
@@ -656,9 +675,8 @@ int maxmin_morph_batched(int dt, const void *in, int64_t batch, int64_t n, int64
   if (out_close && overlap(in, ib, out_close, ob)) return MAXMIN_ERR_ALIAS;
   if (out_open && out_close && overlap(out_open, ob, out_close, ob)) return MAXMIN_ERR_ALIAS;
   int rc;
-  if ((rc = ensure_device(in)) != MAXMIN_OK) return rc;
-  if (out_open && (rc = ensure_device(out_open)) != MAXMIN_OK) return rc;
-  if (out_close && (rc = ensure_device(out_close)) != MAXMIN_OK) return rc;
+  DeviceScope dev;
+  if ((rc = dev.bind({in, out_open, out_close})) != MAXMIN_OK) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   MM_DISPATCH(dt, return mm::launch_morph<T>(in, batch, n, in_ld, w, out_open, out_close, out_ld, s))
 }
@@ -702,10 +720,8 @@ int maxmin_morph_2d(int dt, const void *in, int64_t batch, int64_t rows, int64_t
   for (int i = 0; i < 4; ++i)
     for (int k = i + 1; k < 4; ++k)
       if (regs[i] && regs[k] && overlap(regs[i], rb[i], regs[k], rb[k])) return MAXMIN_ERR_ALIAS;
-  if ((rc = ensure_device(in)) != MAXMIN_OK) return rc;
-  if (out_open && (rc = ensure_device(out_open)) != MAXMIN_OK) return rc;
-  if (out_close && (rc = ensure_device(out_close)) != MAXMIN_OK) return rc;
-  if ((rc = ensure_device(workspace)) != MAXMIN_OK) return rc;
+  DeviceScope dev;
+  if ((rc = dev.bind({in, out_open, out_close, workspace})) != MAXMIN_OK) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   MM_DISPATCH(dt, return mm::launch_morph_2d<T>(in, batch, rows, cols, in_ld, in_bstride, w_row, w_col, out_open,
                                                 out_close, out_ld, out_bstride, workspace, s))
@@ -756,10 +772,8 @@ int maxmin_filter_3d(int dt, const void *in, int64_t depth, int64_t rows, int64_
   for (int i = 0; i < 4; ++i)
     for (int k = i + 1; k < 4; ++k)
       if (regs[i] && regs[k] && overlap(regs[i], rb[i], regs[k], rb[k])) return MAXMIN_ERR_ALIAS;
-  if ((rc = ensure_device(in)) != MAXMIN_OK) return rc;
-  if (out_max && (rc = ensure_device(out_max)) != MAXMIN_OK) return rc;
-  if (out_min && (rc = ensure_device(out_min)) != MAXMIN_OK) return rc;
-  if ((rc = ensure_device(workspace)) != MAXMIN_OK) return rc;
+  DeviceScope dev;
+  if ((rc = dev.bind({in, out_max, out_min, workspace})) != MAXMIN_OK) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   MM_DISPATCH(dt, return mm::launch_3d<T>(in, depth, rows, cols, in_ld, in_slice, w_x, w_y, w_z, out_max, out_min,
                                           out_ld, out_slice, workspace, s))
@@ -797,7 +811,8 @@ int maxmin_filter_1d_host(int dt, const void *in, int64_t n, int64_t w, void *ou
   int rc = maxmin_host_workspace_bytes(dt, n, w, chunk, &need);
   if (rc) return rc;
   if (!dev_ws || ws_bytes < need || !aligned16(dev_ws)) return MAXMIN_ERR_WORKSPACE;
-  if ((rc = ensure_device(dev_ws)) != MAXMIN_OK) return rc;
+  DeviceScope dev;
+  if ((rc = dev.bind({dev_ws})) != MAXMIN_OK) return rc;
   const int64_t m = n - w + 1;
   int64_t c = default_chunk(chunk);
   if (c > m) c = m;
@@ -805,12 +820,23 @@ int maxmin_filter_1d_host(int dt, const void *in, int64_t n, int64_t w, void *ou
   maxmin_workspace_bytes(dt, 1, c + w - 1, w, &kws);
   auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t per = need / 2;
-  cudaStream_t st[2] = {nullptr, nullptr};
-  for (auto &s : st)
-    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
-      rc = mm::note_cuda(cudaGetLastError());
-      break;
+  // two non-blocking streams per (thread, device), created on first use and
+  // kept: creating and destroying them cost more than a small call
+  thread_local std::map<int, std::pair<cudaStream_t, cudaStream_t>> pool;
+  int dev_id = 0;
+  cudaError_t ge = cudaGetDevice(&dev_id);
+  if (ge != cudaSuccess) return mm::note_cuda(ge);
+  auto pit = pool.find(dev_id);
+  if (pit == pool.end()) {
+    cudaStream_t a = nullptr, b = nullptr;
+    if ((ge = cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking)) != cudaSuccess) return mm::note_cuda(ge);
+    if ((ge = cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking)) != cudaSuccess) {
+      cudaStreamDestroy(a);
+      return mm::note_cuda(ge);
     }
+    pit = pool.emplace(dev_id, std::make_pair(a, b)).first;
+  }
+  cudaStream_t st[2] = {pit->second.first, pit->second.second};
   const char *hin = static_cast<const char *>(in);
   int64_t k = 0;
   for (int64_t j0 = 0; j0 < m && rc == MAXMIN_OK; j0 += c, ++k) {
@@ -839,10 +865,8 @@ int maxmin_filter_1d_host(int dt, const void *in, int64_t n, int64_t w, void *ou
     }
   }
   for (auto &s : st) {
-    if (!s) continue;
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess && rc == MAXMIN_OK) rc = mm::note_cuda(e);
-    cudaStreamDestroy(s);
   }
   return rc;
 }

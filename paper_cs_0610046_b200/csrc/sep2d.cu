@@ -110,7 +110,9 @@ int launch_2d_sep(const void *in, int64_t batch, int64_t rows, int64_t cols, int
                          sm_count(), s);
   }
   // the 1-D kernels stage rows with TMA: 16-B aligned rows
-  if ((reinterpret_cast<uintptr_t>(in) & 15) || ((in_ld * (int64_t)sizeof(T)) & 15)) return kErrUnsupported;
+  if ((reinterpret_cast<uintptr_t>(in) & 15) || ((in_ld * (int64_t)sizeof(T)) & 15) ||
+      (batch > 1 && ((in_bstride * (int64_t)sizeof(T)) & 15)))
+    return kErrUnsupported;
   T *tmax = static_cast<T *>(ws);
   T *tmin = reinterpret_cast<T *>(static_cast<char *>(ws) + L.one);
   int rc;

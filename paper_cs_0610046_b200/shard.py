@@ -72,7 +72,7 @@ def tail_start(n_local: int, w: int, align: int = 64) -> int:
     return first_remote // align * align
 
 
-def filter_1d_sharded(buf: torch.Tensor, chunk: Chunk1D, windows, outs, filter_fn, group=None):
+def filter_1d_sharded(buf: torch.Tensor, chunk: Chunk1D, windows, outs, filter_fn, group=None, exchange=None):
     """Run the 1-D filter for each w in `windows` on this rank's chunk.
 
     buf:    1-D tensor with capacity >= n_local + halo; buf[:n_local] is the
@@ -80,10 +80,16 @@ def filter_1d_sharded(buf: torch.Tensor, chunk: Chunk1D, windows, outs, filter_f
     outs:   dict w -> (out_max, out_min) tensors of length >= chunk.windows(w).
     filter_fn(x, w, out_max, out_min): computes the filter of the 1-D tensor x
             into the given output views.
+    exchange(buf, n_local, halo, group) -> requests: the halo transport
+            (default exchange_halo, torch.distributed point-to-point).
     Interior windows run while the halo is in flight; the tail waits for it.
+    This is the protocol of the C ABI's maxmin_filter_1d_sharded (which the
+    product calls with NCCL), written over torch.distributed so that it runs
+    under gloo on CPU.
     """
     n = chunk.n_local
-    reqs = exchange_halo(buf, n, chunk.halo, group) if chunk.world > 1 else []
+    exchange = exchange_halo if exchange is None else exchange
+    reqs = exchange(buf, n, chunk.halo, group) if chunk.world > 1 else []
     for w in windows:  # interior: windows entirely inside the own chunk
         m_int = n - w + 1
         if m_int > 0:
@@ -99,6 +105,23 @@ def filter_1d_sharded(buf: torch.Tensor, chunk: Chunk1D, windows, outs, filter_f
         ox, on = outs[w]
         filter_fn(buf[s:n + w - 1], w, None if ox is None else ox[s:s + m_tail],
                   None if on is None else on[s:s + m_tail])
+
+
+def nccl_comm_ptr(device, group=None) -> int:
+    """The ncclComm_t of torch's NCCL process group on `device`, as an int, for
+    maxmin_filter_1d_sharded (the group must be initialised with device_id so the
+    communicator exists before the first collective)."""
+    from torch.distributed import distributed_c10d as c10d
+
+    pg = group if group is not None else c10d._get_default_group()
+    backend = pg._get_backend(torch.device(device))
+    ptr = backend._comm_ptr()
+    if not ptr:
+        dist.barrier()  # a lazily created communicator exists after the first collective
+        ptr = backend._comm_ptr()
+    if not ptr:
+        raise RuntimeError("no NCCL communicator for this process group")
+    return int(ptr)
 
 
 def cuda_filter_into(x: torch.Tensor, w: int, out_max, out_min, workspace=None) -> None:

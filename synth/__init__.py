@@ -107,6 +107,51 @@ def random_values(dtype, n: int, seed: int, stream: int = 0, alphabet: int | Non
     return (raw >> np.uint64(64 - bits)).astype(np.dtype(f"u{dt.itemsize}")).view(dt)
 
 
+def special_pool(dtype) -> np.ndarray:
+    """The values a comparison kernel is most likely to get wrong for a dtype: the
+    type's extremes and, for floats, +-inf, subnormals (flushed under FTZ), the
+    smallest normals, +-1 and 0 -- never NaN and never -0 (BASELINE.json:5)."""
+    dt = np.dtype(dtype)
+    if dt.kind == "f":
+        fi = np.finfo(dt)
+        tiny_sub = np.array(fi.smallest_subnormal, dt)
+        v = [-np.inf, np.inf, fi.max, -fi.max, fi.tiny, -fi.tiny, tiny_sub, -tiny_sub, tiny_sub * 7,
+             -(tiny_sub * 7), fi.tiny / 2, -(fi.tiny / 2), 0.0, 1.0, -1.0, fi.eps, 1.0 + fi.eps]
+        return np.array(v, dt)
+    ii = np.iinfo(dt)
+    v = {ii.min, ii.max, ii.min + 1, ii.max - 1, 0, 1}
+    if ii.min < 0:
+        v.add(-1)
+    return np.array(sorted(v), dt)
+
+
+def edge_values(dtype, n: int, seed: int, stream: int = 0) -> np.ndarray:
+    """Seeded edge-case series: runs of values drawn from special_pool(dtype) (run
+    lengths 1..64, and every 7th run 500..3000 long: long equal runs), mixed with
+    runs of ordinary random values of the dtype."""
+    dt = np.dtype(dtype)
+    pool = special_pool(dt)
+    raw = raw_u64(seed, stream, 4 * (n // 8 + 16))
+    ordinary = random_values(dt, n, seed + 1, stream)
+    out = np.empty(n, dt)
+    i = k = 0
+    while i < n:
+        r = int(raw[k % raw.shape[0]]); k += 1
+        length = 500 + r % 2500 if k % 7 == 0 else 1 + (r >> 8) % 64
+        length = min(length, n - i)
+        if (r >> 20) % 4 == 0:  # a run of ordinary values
+            out[i:i + length] = ordinary[i:i + length]
+        elif (r >> 20) % 4 == 1:  # distinct specials, one per position
+            idx = raw[(k + np.arange(length)) % raw.shape[0]] % np.uint64(pool.shape[0])
+            out[i:i + length] = pool[idx.astype(np.int64)]
+        else:  # a constant run of one special
+            out[i:i + length] = pool[(r >> 24) % pool.shape[0]]
+        i += length
+    if dt.kind == "f":
+        out[out == 0] = 0  # no -0
+    return out
+
+
 # ---- BASELINE workloads -----------------------------------------------------
 
 def c1(out=None) -> np.ndarray:

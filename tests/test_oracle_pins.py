@@ -574,3 +574,32 @@ def test_3d_vs_numpy_and_2d():
     m2x, m2n = oracle.separable_2d(a, 5, 4)  # w_z = 1 is the 2-D filter of every slice
     m3x, m3n = oracle.separable_3d(a, 5, 4, 1)
     assert same(m2x, m3x) and same(m2n, m3n)
+
+
+def test_oracle_on_edge_values_vs_numpy():
+    """Extremes, +-inf, subnormals and long equal runs: the oracle's streaming
+    variants equal numpy's sliding-window max/min bit for bit."""
+    import synth
+
+    for dt in (np.uint8, np.int8, np.int16, np.uint32, np.int64, np.float32, np.float64):
+        a = synth.edge_values(dt, 30_000, seed=9)
+        for w in (1, 2, 3, 17, 300, 4000):
+            win = swv(a, w)
+            ex, en = win.max(axis=1), win.min(axis=1)
+            for f in (oracle.appendix, oracle.alg1) if w >= 2 else (oracle.appendix,):
+                mx, mn, _ = f(a, w)
+                assert np.array_equal(mx.view(f"u{a.dtype.itemsize}"), ex.view(f"u{a.dtype.itemsize}")), (dt, w)
+                assert np.array_equal(mn.view(f"u{a.dtype.itemsize}"), en.view(f"u{a.dtype.itemsize}")), (dt, w)
+
+
+def test_appendix_baseline_build_equals_oracle():
+    """The CPU-baseline build (-O3 -march=native, threads over window ranges) computes
+    what the pinned oracle computes."""
+    import synth
+
+    a = synth.c5(1_000_003)
+    for w in (1, 7, 4096, 262144):
+        ex, en, _ = oracle.appendix(a, w)
+        for th in (1, 3, 8):
+            mx, mn = oracle.appendix_baseline(a, w, th)
+            assert np.array_equal(mx, ex) and np.array_equal(mn, en), (w, th)

@@ -30,7 +30,18 @@ def oracle_filter_into(x, w, ox, on):
         on.copy_(torch.from_numpy(mn))
 
 
-def _worker(rank, world, port, n_total, windows, q):
+def shifted_exchange(buf, n_local, halo, group=None):
+    """Mutant transport: every rank sends its elements [1, halo+1) instead of [0, halo)."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    ops = []
+    if rank > 0:
+        ops.append(dist.P2POp(dist.isend, buf[1:halo + 1].clone(), rank - 1))
+    if rank < world - 1:
+        ops.append(dist.P2POp(dist.irecv, buf[n_local:n_local + halo], rank + 1))
+    return dist.batch_isend_irecv(ops) if ops else []
+
+
+def _worker(rank, world, port, n_total, windows, q, mutant=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -45,8 +56,18 @@ def _worker(rank, world, port, n_total, windows, q):
         buf[: chunk.n_local] = torch.from_numpy(a[c0:c1])
         outs = {w: (torch.full((chunk.windows(w),), -1.0), torch.full((chunk.windows(w),), -1.0))
                 for w in windows}
-        shard.filter_1d_sharded(buf, chunk, windows, outs, oracle_filter_into)
+        shard.filter_1d_sharded(buf, chunk, windows, outs, oracle_filter_into,
+                                exchange=shifted_exchange if mutant else None)
         dist.barrier()  # every rank has its halo before any rank tears down
+        if mutant:  # the seam windows of every rank but the last must now be wrong
+            bad = 0
+            for w in windows:
+                ex, en, _ = oracle.appendix(a, w)
+                ox, on = outs[w]
+                m = chunk.windows(w)
+                bad += int((ox.numpy() != ex[c0: c0 + m]).sum() + (on.numpy() != en[c0: c0 + m]).sum())
+            q.put((rank, "ok" if (bad > 0) == (rank < world - 1) else f"mutant undetected: {bad}"))
+            return
         # the received halo is the next rank's first w_max-1 elements
         if rank < world - 1:
             assert torch.equal(buf[chunk.n_local: chunk.n_local + halo], torch.from_numpy(a[c1: c1 + halo]))
@@ -74,6 +95,20 @@ def test_sharded_1d_halo_gloo(world):
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(v == "ok" for v in res.values()), res
+
+
+def test_sharded_1d_wrong_halo_is_detected_gloo():
+    """A halo shifted by one element (a plausible transport bug) changes seam windows."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, 100_000 + 5, (32, 1024), q, True)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
     for p in procs:
         p.join(timeout=60)
     assert all(v == "ok" for v in res.values()), res

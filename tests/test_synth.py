@@ -51,3 +51,20 @@ def test_c5_structure():
     d = np.diff(a.astype(np.float64))
     # long strictly monotone runs of step exactly +1 / -1
     assert (d == 1).mean() > 0.15 and (d == -1).mean() > 0.15
+
+
+def test_edge_values_structure():
+    """Edge-case series: every special of the dtype occurs, no NaN / -0, long equal
+    runs, deterministic."""
+    for dt in (np.uint8, np.int8, np.uint16, np.int16, np.uint32, np.int32, np.uint64, np.int64,
+               np.float32, np.float64):
+        a = synth.edge_values(dt, 200_000, seed=5)
+        assert a.dtype == np.dtype(dt) and a.shape == (200_000,)
+        assert np.array_equal(a, synth.edge_values(dt, 200_000, seed=5))
+        pool = synth.special_pool(dt)
+        assert np.isin(pool, a).all(), np.dtype(dt).name
+        if np.dtype(dt).kind == "f":
+            _no_nan_no_negzero(a)
+            assert np.isinf(a).any() and (np.abs(a[np.isfinite(a)]) < np.finfo(dt).tiny).any()
+        runs = np.flatnonzero(np.diff(a.view(f"u{a.dtype.itemsize}")) != 0)
+        assert np.diff(runs).max() >= 500  # a long constant run
