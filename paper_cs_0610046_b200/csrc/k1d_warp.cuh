@@ -34,6 +34,10 @@
 
 #include "k1d_large.cuh"
 
+#ifndef MM_WARP_CONTIG  // 1: one contiguous group range per CTA (round 1); 0: round-robin groups
+#define MM_WARP_CONTIG 0
+#endif
+
 namespace mm {
 
 template <typename T>
@@ -143,6 +147,7 @@ __global__ void __launch_bounds__(NT, MM_WARP_MINB)
   const int hstart = WT - g.r;              // H range of a far chunk: [hstart, WT)
   const int h_lane = hstart / E, h_off = hstart % E;
 
+#if MM_WARP_CONTIG
   // this CTA's groups [gbeg, gend), and the prologue groups [pbeg, gbeg) of
   // the same row that its first gaps reach into
   const int64_t gbeg = g.total * (int64_t)blockIdx.x / gridDim.x;
@@ -150,6 +155,21 @@ __global__ void __launch_bounds__(NT, MM_WARP_MINB)
   if (gbeg >= gend) return;
   const int64_t row0 = gbeg / g.kt;
   const int64_t pbeg = gbeg - row0 * g.kt >= g.pg ? gbeg - g.pg : row0 * g.kt;
+  constexpr int64_t gstep = 1;
+#else
+  // groups dealt round-robin: CTA b takes b, b + grid, b + 2 grid, ...  The
+  // whole grid sweeps the rows as one front, so the near chunk of tile x is
+  // read shortly after the far chunk of tile x-q loaded the same bytes (an L2
+  // hit), and every group -- the publish-only ones at row starts included --
+  // has an owner: no prologue.  Gaps reach into groups of other CTAs; the
+  // launch is cooperative (every CTA resident), and a CTA only ever waits on
+  // groups below the one it processes, so the lowest unpublished group's owner
+  // can always proceed.
+  const int64_t gbeg = blockIdx.x, gend = g.total, pbeg = gbeg;
+  if (gbeg >= gend) return;
+  const int64_t gstep = gridDim.x;
+  const int64_t step_rows = gstep / g.kt, step_x = (gstep - step_rows * g.kt) * K;
+#endif
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NWARP * Geo::NBAR; ++i) mbar_init(reinterpret_cast<uint64_t *>(tail) + i, 1);
@@ -173,6 +193,7 @@ __global__ void __launch_bounds__(NT, MM_WARP_MINB)
     q_.x = -g.q + (int)(tk - q_.row * g.kt) * K + warp;
     return q_;
   };
+#if MM_WARP_CONTIG
   auto advance = [&](Pos &q_) {
     ++q_.tk;
     q_.x += K;
@@ -181,6 +202,17 @@ __global__ void __launch_bounds__(NT, MM_WARP_MINB)
       q_.x = -g.q + warp;
     }
   };
+#else
+  auto advance = [&](Pos &q_) {
+    q_.tk += gstep;
+    q_.row += step_rows;
+    q_.x += (int)step_x;
+    if (q_.x >= xend + warp) {
+      ++q_.row;
+      q_.x -= (int)g.kt * K;
+    }
+  };
+#endif
   auto exists = [&](const Pos &q_) { return q_.tk < gend && q_.x < g.tpr; };
   // lane 0: TMA loads of a job's far chunk / near chunk (an absent tile arms
   // the barrier with nothing in flight)

@@ -370,10 +370,27 @@ static int launch_warp(const Rows &p, void *ws, size_t ws_bytes, cudaStream_t s)
     rc = raise_smem_limit(reinterpret_cast<const void *>(kern), smem);
     if (rc) return rc;
     int grid = 0;
+#if MM_WARP_CONTIG
     rc = occupancy_grid(kern, smem, (g.total + NWARP - 1) / NWARP, grid);
     if (rc) return rc;
     kern<<<grid, NT, smem, s>>>(p, g, ws, map);
     return note_cuda(cudaGetLastError());
+#else
+    // every CTA resident (cooperative launch): gaps wait on other CTAs' groups
+    rc = occupancy_grid(kern, smem, g.total, grid);
+    if (rc) return rc;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return note_cuda(cudaLaunchKernelEx(&cfg, kern, p, g, ws, map));
+#endif
   }
 }
 
