@@ -8,3 +8,4 @@
 #include "k1d_medium.cuh"
 #include "k1d_large.cuh"
 #include "k1d_warp.cuh"
+#include "k1d_lw.cuh"

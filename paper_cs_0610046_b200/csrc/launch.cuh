@@ -105,7 +105,8 @@ int launch_morph_2d(const void *in, int64_t batch, int64_t rows, int64_t cols, i
 int encode_u8_map(CUtensorMap *map, const void *base, const int64_t dims[3], const int64_t strides[2],
                   const int box[3]);  // maxmin_abi.cu
 int encode_rows_map(CUtensorMap *map, const void *in, int elem_bytes, int64_t rows_per_series,
-                    int64_t batch, int64_t in_ld_bytes, int box_rows = kBoxRows);  // maxmin_abi.cu
+                    int64_t batch, int64_t in_ld_bytes, int box_rows = kBoxRows,
+                    bool swizzle = true);  // maxmin_abi.cu
 
 // Tile geometry of the 1-D kernels for element type T.
 template <typename T>
@@ -148,11 +149,31 @@ WarpLB warp_geom(int64_t batch, int64_t n, int64_t w) {
   return g;
 }
 
+#ifndef MM_LW  // 1: the large-window path of <= 4-byte types is k1d_lw; 0: k1d_warp (round 1)
+#define MM_LW 1
+#endif
+
+template <typename T>
+LwArgs lw_geom(int64_t batch, int64_t n, int64_t w) {
+  LwArgs g{};
+  if constexpr (sizeof(T) <= 4) {
+    constexpr int64_t WT = LwGeo<T>::WT;
+    const int64_t m = n - w + 1;
+    g.q = (int)((w - 1) / WT);
+    g.r = (int)((w - 1) % WT);
+    g.tpr = (m + WT - 1) / WT;
+    g.kt = (g.q + g.tpr + NWARP - 1) / NWARP;
+    g.total = batch * g.kt;
+  }
+  return g;
+}
+
 template <typename T>
 size_t workspace_1d(int64_t batch, int64_t n, int64_t w) {
   if (batch == 0) return 0;
   if constexpr (sizeof(T) <= 4) {
-    if (path_1d<T>(w) == Path1D::Warp) return WarpWs<T>::bytes(warp_geom<T>(batch, n, w), batch);
+    if (path_1d<T>(w) == Path1D::Warp)
+      return MM_LW ? LwWs<T>::bytes(lw_geom<T>(batch, n, w)) : WarpWs<T>::bytes(warp_geom<T>(batch, n, w), batch);
   }
   if (path_1d<T>(w) != Path1D::Large) return 0;
   const int64_t TILE = Geo1D<T>::TILE;
@@ -335,9 +356,55 @@ static int launch_large(const Rows &p, const CUtensorMap &small, void *ws, size_
 }
 
 template <typename T>
+static int launch_lw(const Rows &p, void *ws, size_t ws_bytes, cudaStream_t s) {
+  if constexpr (sizeof(T) > 4) {
+    return kErrUnsupported;
+  } else {
+    using Geo = LwGeo<T>;
+    // maps over the whole 128-B rows: chunks {RW, NROWS} (near chunks, the far
+    // chunks' first NROWS rows) and single unswizzled rows (the far chunks' last)
+    TmaMaps map;
+    std::memset(&map, 0, sizeof(map));
+    const int64_t full_rows = p.n / Rowing<T>::RW;
+    int rc = encode_rows_map(&map.big, p.in, (int)sizeof(T), full_rows, p.batch,
+                             p.in_ld * (int64_t)sizeof(T), Geo::NROWS);
+    if (!rc)  // the far chunk's last row: one unswizzled row
+      rc = encode_rows_map(&map.small, p.in, (int)sizeof(T), full_rows, p.batch,
+                           p.in_ld * (int64_t)sizeof(T), 1, false);
+    if (rc) return rc;
+    const LwArgs g = lw_geom<T>(p.batch, p.n, p.w);
+    if (!ws || ws_bytes < LwWs<T>::bytes(g)) return kErrWorkspace;
+    if (g.total > 0x7fffffffLL) return kErrUnsupported;
+    // every word's flag: one memset (256 B per 4096 outputs)
+    cudaError_t e = cudaMemsetAsync(ws, 0, LwWs<T>::bytes(g), s);
+    if (e != cudaSuccess) return note_cuda(e);
+    // the far chunk's in-vector shift is a template parameter for 4-byte types
+    auto kern = k1d_lw<T, -1>;
+    if constexpr (sizeof(T) == 4) {
+      switch ((int)((p.w - 1) % Geo::VEC)) {
+        case 0: kern = k1d_lw<T, 0>; break;
+        case 1: kern = k1d_lw<T, 1>; break;
+        case 2: kern = k1d_lw<T, 2>; break;
+        default: kern = k1d_lw<T, 3>; break;
+      }
+    }
+    constexpr size_t smem = Geo::BYTES;
+    rc = raise_smem_limit(reinterpret_cast<const void *>(kern), smem);
+    if (rc) return rc;
+    int grid = 0;
+    rc = occupancy_grid(kern, smem, g.total, grid);
+    if (rc) return rc;
+    kern<<<grid, NT, smem, s>>>(p, g, ws, map);  // groups by ticket: no residency assumption
+    return note_cuda(cudaGetLastError());
+  }
+}
+
+template <typename T>
 static int launch_warp(const Rows &p, void *ws, size_t ws_bytes, cudaStream_t s) {
   if constexpr (sizeof(T) > 4) {
     return kErrUnsupported;
+  } else if (MM_LW) {
+    return launch_lw<T>(p, ws, ws_bytes, s);
   } else {
     using Geo = WarpGeo<T>;
     // maps over the whole 128-B rows: near chunks {RW, 16} and far chunks {RW, 17}

@@ -54,7 +54,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // 3-D map {RW, rows_per_series, batch} of 128-byte rows, boxes {RW, 8, 1},
 // 128-byte swizzle, zero fill out of bounds (tma.cuh).
 int encode_rows_map(CUtensorMap *map, const void *in, int elem_bytes, int64_t rows_per_series,
-                    int64_t batch, int64_t in_ld_bytes, int box_rows) {
+                    int64_t batch, int64_t in_ld_bytes, int box_rows, bool swizzle) {
   auto fn = encode_fn();
   if (!fn) return note_cuda(cudaErrorNotSupported);
   CUtensorMapDataType dt = elem_bytes == 1   ? CU_TENSOR_MAP_DATA_TYPE_UINT8
@@ -67,7 +67,7 @@ int encode_rows_map(CUtensorMap *map, const void *in, int elem_bytes, int64_t ro
   cuuint32_t box[3] = {(cuuint32_t)RW, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, dt, 3, const_cast<void *>(in), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return note_cuda(cudaErrorInvalidValue);
   return kOK;
