@@ -47,7 +47,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None,
     lib = out or LIB
     if not force and not defines and out is None and up_to_date():
         return LIB
-    build_dir = BUILD if not defines else BUILD + "_" + "_".join(d.replace("=", "") for d in defines)
+    # variant objects live outside the tree (they would travel with every gpurun snapshot)
+    build_dir = BUILD if not defines else os.path.join("/tmp", "maxmin_obj_" + "_".join(d.replace("=", "") for d in defines))
     os.makedirs(build_dir, exist_ok=True)
     nvcc = _nvcc()
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
