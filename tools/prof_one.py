@@ -25,6 +25,12 @@ if a.config == "C2":
                      dtype=torch.uint8, device=dev)
     for _ in range(a.reps):
         mm.maxmin_filter_1d(x, a.w, workspace=ws)
+elif a.config == "C5":
+    x = torch.from_numpy(synth.c5(1 << 30)).to(dev)
+    ws = torch.empty(max(mm.maxmin_workspace_bytes(torch.float32, 1, x.numel(), a.w), 16),
+                     dtype=torch.uint8, device=dev)
+    for _ in range(a.reps):
+        mm.maxmin_filter_1d(x, a.w, workspace=ws)
 elif a.config == "C3":
     x = torch.from_numpy(synth.c3()).to(dev)
     for _ in range(a.reps):
