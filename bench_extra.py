@@ -20,14 +20,9 @@ def _timed(step, steps, warmup, world, dev):
         dist.barrier()
     torch.cuda.synchronize()
     s = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # clock record over a soak of untimed steps and the timed region (bench.timed_loop)
     with bench.ClockSampler(torch.cuda.current_device()) as clk:
-        e0.record(s)
-        for _ in range(steps):
-            step()
-        e1.record(s)
-        torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+        ms = bench.timed_loop(step, steps, s, clk)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

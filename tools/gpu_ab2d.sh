@@ -1,6 +1,8 @@
-# A/B of 2-D kernel variants: C4 bench for each library given as arguments
+# A/B of 2-D builds on C4 (alternated twice): LIBS="a.so b.so" OUT=dir
 cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out
-for lib in "$@"; do
-  MAXMIN_LIB=$lib timeout 300 python bench.py --config C4 --steps 10 --warmup 3 --no-e2e --no-cpu > gpurun_out/ab2d_$lib.log 2>&1
+mkdir -p gpurun_out/$OUT
+for rep in 1 2; do
+for lib in $LIBS; do
+  MAXMIN_LIB=$lib timeout 300 python tools/time_2d.py --reps 10 >> gpurun_out/$OUT/ab_c4_$lib.log 2>&1
+done
 done
