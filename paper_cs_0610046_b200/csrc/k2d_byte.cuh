@@ -61,9 +61,6 @@ namespace k2b {
 #ifndef MM_K2B_NMID
 #define MM_K2B_NMID 4
 #endif
-#ifndef MM_K2B_COL_DBL  // column pass: 1 = span-doubling plan of 2-input ops, 0 = 3-input sparse table
-#define MM_K2B_COL_DBL 1
-#endif
 
 constexpr int NTB = 256;      // threads per CTA
 constexpr int NRT = 128;      // row-pass threads (warps 0-3)
@@ -111,25 +108,6 @@ __host__ __device__ constexpr Plan make_plan(int W) {
 __host__ __device__ constexpr int plan_K(int W) { return make_plan(W).K; }
 __host__ __device__ constexpr int plan_s(int W, int k) { return make_plan(W).s[k]; }
 __host__ __device__ constexpr int plan_d(int W, int k) { return make_plan(W).d[k]; }
-// Span doubling with 2-input ops: level k+1 of span s' = min(2s, W) is
-// op(M_s[j], M_s[j+s'-s]).  A 3-input VIMNMX3 issues at half the rate of the
-// 2-input form (tools/micro/pipes.cu: FMNMX3 65 vs 132 thread-ops per clock
-// per SM), so for W=15 the four 2-input levels (1 -> 2 -> 4 -> 8 -> 15) cost
-// 4 issue slots per output against 6 for the three 3-input ones.
-__host__ __device__ constexpr Plan make_plan2(int W) {
-  Plan p{};
-  p.K = 0;
-  p.s[0] = 1;
-  while (p.s[p.K] < W) {
-    const int s = p.s[p.K];
-    p.s[p.K + 1] = 2 * s < W ? 2 * s : W;
-    p.d[p.K] = 0;
-    ++p.K;
-  }
-  return p;
-}
-__host__ __device__ constexpr int plan2_K(int W) { return make_plan2(W).K; }
-__host__ __device__ constexpr int plan2_s(int W, int k) { return make_plan2(W).s[k]; }
 
 template <int WR>
 struct RowGeo {
@@ -269,22 +247,6 @@ struct ColRing {
 
 // Feed one new value A_0[t]; returns A_K[t] = op over the last W values (valid
 // once W values have been fed since the start of a tile).
-#if MM_K2B_COL_DBL
-template <int W, bool MAX, int k = 0>
-__device__ __forceinline__ uint32_t ring_push(ColRing<W> &r, uint32_t cur) {
-  if constexpr (k < plan2_K(W)) {
-    constexpr int a = plan2_s(W, k + 1) - plan2_s(W, k);
-    constexpr int o = plan2_s(W, k) - 1;  // level k's history: h[o .. o+a) = A_k[t-a .. t-1]
-    const uint32_t nxt = MAX ? vmx(r.h[o], cur) : vmn(r.h[o], cur);  // A_{k+1}[t] = op(A_k[t-a], A_k[t])
-#pragma unroll
-    for (int i = 0; i + 1 < a; ++i) r.h[o + i] = r.h[o + i + 1];
-    r.h[o + a - 1] = cur;
-    return ring_push<W, MAX, k + 1>(r, nxt);
-  } else {
-    return cur;
-  }
-}
-#else
 template <int W, bool MAX, int k = 0>
 __device__ __forceinline__ uint32_t ring_push(ColRing<W> &r, uint32_t cur) {
   if constexpr (k < plan_K(W)) {
@@ -302,7 +264,6 @@ __device__ __forceinline__ uint32_t ring_push(ColRing<W> &r, uint32_t cur) {
     return cur;
   }
 }
-#endif
 
 template <bool SIGNED, int WR, int WC>
 __global__ void __launch_bounds__(NTB, 2) k2d_byte(Args p, const __grid_constant__ CUtensorMap in_map) {
