@@ -171,6 +171,9 @@ struct StoreEpi {
   }
 };
 
+#ifndef MM_WARP_E
+#define MM_WARP_E 16
+#endif
 // max/min of v[o..E-1] for a warp-uniform (or single-lane) runtime o in [0, E)
 template <typename T, int E>
 __device__ __forceinline__ void suffix_from(const T (&v)[E], int o, T &hx, T &hn) {
@@ -186,6 +189,11 @@ __device__ __forceinline__ void suffix_from(const T (&v)[E], int o, T &hx, T &hn
     MM_SUF_CASE(0) MM_SUF_CASE(1) MM_SUF_CASE(2) MM_SUF_CASE(3) MM_SUF_CASE(4) MM_SUF_CASE(5)
     MM_SUF_CASE(6) MM_SUF_CASE(7) MM_SUF_CASE(8) MM_SUF_CASE(9) MM_SUF_CASE(10) MM_SUF_CASE(11)
     MM_SUF_CASE(12) MM_SUF_CASE(13) MM_SUF_CASE(14) MM_SUF_CASE(15)
+#if MM_WARP_E > 16
+    MM_SUF_CASE(16) MM_SUF_CASE(17) MM_SUF_CASE(18) MM_SUF_CASE(19) MM_SUF_CASE(20) MM_SUF_CASE(21)
+    MM_SUF_CASE(22) MM_SUF_CASE(23) MM_SUF_CASE(24) MM_SUF_CASE(25) MM_SUF_CASE(26) MM_SUF_CASE(27)
+    MM_SUF_CASE(28) MM_SUF_CASE(29) MM_SUF_CASE(30) MM_SUF_CASE(31)
+#endif
     default: break;
   }
 #undef MM_SUF_CASE

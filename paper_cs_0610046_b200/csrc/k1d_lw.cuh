@@ -139,8 +139,12 @@ __device__ __forceinline__ uint64_t lw_wait(const uint64_t *s, LwStats &st) {
 #endif
 }
 
+#ifndef MM_LW_MINB  // resident CTAs per SM the register budget is sized for
+#define MM_LW_MINB 2
+#endif
+
 template <typename T, int SH>
-__global__ void __launch_bounds__(NT, 2) k1d_lw(Rows p, LwArgs g, void *ws, const __grid_constant__ TmaMaps maps) {
+__global__ void __launch_bounds__(NT, MM_LW_MINB) k1d_lw(Rows p, LwArgs g, void *ws, const __grid_constant__ TmaMaps maps) {
   using Geo = LwGeo<T>;
   constexpr int E = Geo::E, WT = Geo::WT, RW = Geo::RW;
   extern __shared__ __align__(1024) unsigned char smem_raw[];

@@ -258,11 +258,14 @@ static int launch_small_dispatch(const Rows &p, const CUtensorMap &map, cudaStre
 // Block geometry of k1d_medium: B = E*G, the largest power of two <= w-1 with
 // 1 <= G <= 32; D = w-1-B = q'B + r'.
 // Lanes per block of k1d_medium: the largest power of two G <= 32 with E*G <= w-1.
+#ifndef MM_MED_GMAX  // largest group (lanes per block) of k1d_medium
+#define MM_MED_GMAX 32
+#endif
 template <typename T>
 int medium_G(int64_t w) {
   constexpr int E = Chunk<T>::E;
   int G = 1;
-  while (G < 32 && (int64_t)E * G * 2 <= w - 1) G *= 2;
+  while (G < MM_MED_GMAX && (int64_t)E * G * 2 <= w - 1) G *= 2;
   return G;
 }
 
