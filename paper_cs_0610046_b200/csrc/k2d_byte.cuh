@@ -133,6 +133,7 @@ struct Args {
   int64_t nbands;     // bands per image
   int64_t ntiles;     // batch * nbands * nstrip
   uint32_t one, k8, k16, k24;  // 1, 1 << 8, 1 << 16, 1 << 24 (opaque to the compiler)
+  int in_r0;  // input row of output row 0's first window row: 0, or -(w-1) for a framed input (morphology)
 };
 
 // packed 16x2 max/min (the 3-input form is formed by ptxas)
@@ -265,7 +266,17 @@ __device__ __forceinline__ uint32_t ring_push(ColRing<W> &r, uint32_t cur) {
   }
 }
 
-template <bool SIGNED, int WR, int WC>
+// FIN: XOR applied to every input byte (0x80 maps i8 to an order-preserving u8);
+// FXO / FNO: XOR applied to the max / min output bytes.  FRAMED: the input is
+// read through a (w-1)-wide zero frame on every side and only the max filter is
+// computed (the min chain, its intermediate and its stores are compiled out):
+// output (r, c) is the max over input rows [r-w+1, r] x columns [c-w+1, c].
+// Row coordinates of the frame are negative tensor-map coordinates; columns
+// start 16 bytes before the strip (a TMA box's inner start must be 16-B
+// aligned), and the row pass reads every item D = 17 - w bytes further in.
+// The plain filter is <0,0,0> (u8) or <0x80,0x80,0x80> (i8); the morphology
+// passes use the others (launch_morph_2d_byte).
+template <uint32_t FIN, uint32_t FXO, uint32_t FNO, bool FRAMED, int WR, int WC>
 __global__ void __launch_bounds__(NTB, 2) k2d_byte(Args p, const __grid_constant__ CUtensorMap in_map) {
   using G = RowGeo<WR>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -274,7 +285,7 @@ __global__ void __launch_bounds__(NTB, 2) k2d_byte(Args p, const __grid_constant
   unsigned char *mid = base + NSTG * STAGE_IN;   // [NMID][2 filters][RB][MP]
   uint64_t *bars = reinterpret_cast<uint64_t *>(mid + NMID * 2 * MID);
   const int tid = threadIdx.x, warp = tid >> 5;
-  constexpr uint32_t FLIP = SIGNED ? 0x80808080u : 0u;
+  constexpr uint32_t FLIP = FIN * 0x01010101u, XOUT = FXO * 0x01010101u, NOUT = FNO * 0x01010101u;
 
   const int64_t G_ = gridDim.x;
   if ((int64_t)blockIdx.x >= p.ntiles) return;
@@ -326,7 +337,7 @@ __global__ void __launch_bounds__(NTB, 2) k2d_byte(Args p, const __grid_constant
     int ld_buf = 0;
     auto issue = [&]() {  // three TMA boxes of 176 columns x RB rows
       unsigned char *dst = stage_in + ld_buf * STAGE_IN;
-      const int r0 = (int)(ld.o0 + ld.st * RB), c0 = (int)ld.c0, b = (int)ld.b;
+      const int r0 = (int)(ld.o0 + ld.st * RB) + p.in_r0, c0 = (int)ld.c0 - (FRAMED ? 16 : 0), b = (int)ld.b;
       mbar_arrive_expect_tx(&bars[ld_buf], (uint32_t)STAGE_IN);  // OOB parts are zero-filled
 #pragma unroll
       for (int k = 0; k < 3; ++k) tma_load3(&in_map, dst + k * INBOX, c0 + k * BOXW, r0, b, &bars[ld_buf]);
@@ -342,9 +353,15 @@ __global__ void __launch_bounds__(NTB, 2) k2d_byte(Args p, const __grid_constant
     // [32g, 32g + 32) of the strip; lanes pr = 0..7 of a quarter-warp touch 8
     // different rows, which the 176/528-byte pitches spread over all banks
     const int pr = tid & 7, g = tid >> 3;
-    int offa[G::NCH], offb[G::NCH];
+    // framed input: the stage starts 16 columns before the strip, the item's
+    // first needed column is D bytes into its first chunk, and 32 + w - 1 + D
+    // = 48 columns are three chunks for every w
+    constexpr int D = FRAMED ? 17 - WR : 0;
+    constexpr int NCHR = FRAMED ? 3 : G::NCH;
+    static_assert(D + G::L <= 16 * NCHR && TW - ER + 16 * NCHR <= INW, "item reads stay inside the stage");
+    int offa[NCHR], offb[NCHR];
 #pragma unroll
-    for (int c = 0; c < G::NCH; ++c) {
+    for (int c = 0; c < NCHR; ++c) {
       offa[c] = in_off(g * ER + 16 * c, pr);
       offb[c] = in_off(g * ER + 16 * c, pr + 8);
     }
@@ -359,49 +376,51 @@ __global__ void __launch_bounds__(NTB, 2) k2d_byte(Args p, const __grid_constant
 #if !MM_K2B_ROW_VHGW
       uint32_t y[G::L];
 #endif
+      uint32_t ra[4 * NCHR], rb[4 * NCHR];
 #pragma unroll
-      for (int c = 0; c < G::NCH; ++c) {
+      for (int c = 0; c < NCHR; ++c) {
         const uint4 va = *reinterpret_cast<const uint4 *>(sb + offa[c]);
         const uint4 vb = *reinterpret_cast<const uint4 *>(sb + offb[c]);
-        const uint32_t ra[4] = {va.x ^ FLIP, va.y ^ FLIP, va.z ^ FLIP, va.w ^ FLIP};
-        const uint32_t rb[4] = {vb.x ^ FLIP, vb.y ^ FLIP, vb.z ^ FLIP, vb.w ^ FLIP};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          // word j: column j of row A in byte 1 (lane 0's high byte), of row B
-          // in byte 3 (bytes 0 and 2 repeat them)
+        ra[4 * c] = va.x ^ FLIP, ra[4 * c + 1] = va.y ^ FLIP, ra[4 * c + 2] = va.z ^ FLIP, ra[4 * c + 3] = va.w ^ FLIP;
+        rb[4 * c] = vb.x ^ FLIP, rb[4 * c + 1] = vb.y ^ FLIP, rb[4 * c + 2] = vb.z ^ FLIP, rb[4 * c + 3] = vb.w ^ FLIP;
+      }
 #if MM_K2B_FMA_UNPACK
-          // the same words built with IMADs (FMA pipe): [0 A0 0 B0], [A0 A1 B0 B1],
-          // [A1 A2 0 B2], [A2 A3 B2 B3] -- bytes 0 and 2 are don't-care
-          const uint32_t a = ra[q], b = rb[q];
-          const uint32_t hb = umulhi(b, p.k16);
-          const uint32_t w[4] = {umad(b, p.k24, umulhi(umul(a, p.k24), p.k16)),
-                                 umad(b, p.k16, umulhi(umul(a, p.k16), p.k16)),
-                                 umad(hb, p.k24, umulhi(umul(a, p.k8), p.k16)),
-                                 umad(hb, p.k16, umulhi(a, p.k16))};
+      static_assert(D == 0, "the IMAD unpack takes unshifted items");
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int j = 16 * c + 4 * q + t;
-            if (j < G::L) x[j] = w[t];
-#if !MM_K2B_ROW_VHGW
-            if (j < G::L) y[j] = w[t];
-#endif
-          }
-#else
+      for (int q = 0; q < 4 * NCHR; ++q) {
+        // the same words built with IMADs (FMA pipe): [0 A0 0 B0], [A0 A1 B0 B1],
+        // [A1 A2 0 B2], [A2 A3 B2 B3] -- bytes 0 and 2 are don't-care
+        const uint32_t a = ra[q], b = rb[q];
+        const uint32_t hb = umulhi(b, p.k16);
+        const uint32_t w[4] = {umad(b, p.k24, umulhi(umul(a, p.k24), p.k16)),
+                               umad(b, p.k16, umulhi(umul(a, p.k16), p.k16)),
+                               umad(hb, p.k24, umulhi(umul(a, p.k8), p.k16)),
+                               umad(hb, p.k16, umulhi(a, p.k16))};
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int j = 16 * c + 4 * q + t;
-            if (j < G::L) x[j] = prmt(ra[q], rb[q], 0x4400u + 0x1111u * (uint32_t)t);
+        for (int t = 0; t < 4; ++t) {
+          const int j = 4 * q + t;
+          if (j < G::L) x[j] = w[t];
 #if !MM_K2B_ROW_VHGW
-            if (j < G::L) y[j] = x[j];
-#endif
-          }
+          if (j < G::L) y[j] = w[t];
 #endif
         }
       }
+#else
+      // word j: column j of row A in byte 1 (lane 0's high byte), of row B in
+      // byte 3 (bytes 0 and 2 repeat them)
+#pragma unroll
+      for (int j = 0; j < G::L; ++j) {
+        const int src = j + D;
+        x[j] = prmt(ra[src / 4], rb[src / 4], 0x4400u + 0x1111u * (uint32_t)(src % 4));
+#if !MM_K2B_ROW_VHGW
+        y[j] = x[j];
+#endif
+      }
+#endif
 #if MM_K2B_ROW_VHGW
-      uint32_t fx[ER], fn[ER];  // column i of the item
+      uint32_t fx[ER], fn[ER] = {};  // column i of the item
       vhgw_row<WR, true>(x, fx);
-      vhgw_row<WR, false>(x, fn);
+      if constexpr (!FRAMED) vhgw_row<WR, false>(x, fn);
       constexpr int F0 = 0;
 #else
       sparse_row<WR, true>(x);
@@ -422,14 +441,18 @@ __global__ void __launch_bounds__(NTB, 2) k2d_byte(Args p, const __grid_constant
           uint32_t P = prmt(fx[j], fx[j + 1], 0x7351u), Q = prmt(fx[j + 2], fx[j + 3], 0x7351u);
           oxa[q] = prmt(P, Q, 0x5410u);
           oxb[q] = prmt(P, Q, 0x7632u);
-          P = prmt(fn[j], fn[j + 1], 0x7351u), Q = prmt(fn[j + 2], fn[j + 3], 0x7351u);
-          ona[q] = prmt(P, Q, 0x5410u);
-          onb[q] = prmt(P, Q, 0x7632u);
+          if constexpr (!FRAMED) {
+            P = prmt(fn[j], fn[j + 1], 0x7351u), Q = prmt(fn[j + 2], fn[j + 3], 0x7351u);
+            ona[q] = prmt(P, Q, 0x5410u);
+            onb[q] = prmt(P, Q, 0x7632u);
+          }
         }
         *reinterpret_cast<uint4 *>(mx_mid + oa + 16 * h) = make_uint4(oxa[0], oxa[1], oxa[2], oxa[3]);
         *reinterpret_cast<uint4 *>(mx_mid + ob + 16 * h) = make_uint4(oxb[0], oxb[1], oxb[2], oxb[3]);
-        *reinterpret_cast<uint4 *>(mn_mid + oa + 16 * h) = make_uint4(ona[0], ona[1], ona[2], ona[3]);
-        *reinterpret_cast<uint4 *>(mn_mid + ob + 16 * h) = make_uint4(onb[0], onb[1], onb[2], onb[3]);
+        if constexpr (!FRAMED) {
+          *reinterpret_cast<uint4 *>(mn_mid + oa + 16 * h) = make_uint4(ona[0], ona[1], ona[2], ona[3]);
+          *reinterpret_cast<uint4 *>(mn_mid + ob + 16 * h) = make_uint4(onb[0], onb[1], onb[2], onb[3]);
+        }
       }
       bar_arrive(kBarFull + mb, NTB);  // hand mid[mb] to the column warps
       bar_sync(kBarRow, NRT);          // every row thread is done with input stage `buf`
@@ -461,8 +484,8 @@ __global__ void __launch_bounds__(NTB, 2) k2d_byte(Args p, const __grid_constant
       // of a stage are ever stored)
       const int64_t o = cs.b * p.out_bstride + (cs.o0 - (WC - 1)) * p.out_ld + c;
       uint8_t *bx = p.out_max ? p.out_max + o : nullptr;
-      uint8_t *bn = p.out_min ? p.out_min + o : nullptr;
-      const bool fast_cols = cl >= 4 && bx && bn;
+      uint8_t *bn = !FRAMED && p.out_min ? p.out_min + o : nullptr;
+      const bool fast_cols = cl >= 4 && bx && (bn || FRAMED);
       for (int st = 0; st < nst; ++st, --left) {
         const unsigned char *mx_mid = mid + (size_t)(2 * mb) * MID + 4 * ct;
         const unsigned char *mn_mid = mx_mid + MID;
@@ -471,13 +494,17 @@ __global__ void __launch_bounds__(NTB, 2) k2d_byte(Args p, const __grid_constant
 #pragma unroll
         for (int r = 0; r < RB; ++r) {
           const uint32_t vx = *reinterpret_cast<const uint32_t *>(mx_mid + r * MP);
-          const uint32_t vn = *reinterpret_cast<const uint32_t *>(mn_mid + r * MP);
           const uint32_t xo = ring_push<WC, true>(rxo, vx);
           const uint32_t xe = ring_push<WC, true>(rxe, vx << 8);
-          const uint32_t no = ring_push<WC, false>(rno, vn);
-          const uint32_t ne = ring_push<WC, false>(rne, vn << 8);
-          wx[r] = prmt(xe, xo, 0x7351u) ^ FLIP;
-          wn[r] = prmt(ne, no, 0x7351u) ^ FLIP;
+          wx[r] = prmt(xe, xo, 0x7351u) ^ XOUT;
+          if constexpr (!FRAMED) {
+            const uint32_t vn = *reinterpret_cast<const uint32_t *>(mn_mid + r * MP);
+            const uint32_t no = ring_push<WC, false>(rno, vn);
+            const uint32_t ne = ring_push<WC, false>(rne, vn << 8);
+            wn[r] = prmt(ne, no, 0x7351u) ^ NOUT;
+          } else {
+            wn[r] = 0;
+          }
         }
         // mid[mb] has been read: release it (only if the row side will wait for it)
         if (left > NMID) bar_arrive(kBarEmpty + mb, NTB);
@@ -491,9 +518,9 @@ __global__ void __launch_bounds__(NTB, 2) k2d_byte(Args p, const __grid_constant
 #pragma unroll
           for (int r = 0; r < RB; ++r) {
             st_u32(ax, wx[r]);
-            st_u32(an, wn[r]);
+            if constexpr (!FRAMED) st_u32(an, wn[r]);
             ax = ptr_step(ax, one, ld);
-            an = ptr_step(an, one, ld);
+            if constexpr (!FRAMED) an = ptr_step(an, one, ld);
           }
         } else if (cl > 0) {  // partial stage or ragged right edge: byte stores
           const int ncol = (int)(cl < 4 ? cl : 4);
@@ -502,7 +529,7 @@ __global__ void __launch_bounds__(NTB, 2) k2d_byte(Args p, const __grid_constant
             if (r < r_lo || r >= r_hi) continue;
             for (int k = 0; k < ncol; ++k) {
               if (p.out_max) bx[(int64_t)r * p.out_ld + k] = (uint8_t)(wx[r] >> (8 * k));
-              if (p.out_min) bn[(int64_t)r * p.out_ld + k] = (uint8_t)(wn[r] >> (8 * k));
+              if (!FRAMED && p.out_min) bn[(int64_t)r * p.out_ld + k] = (uint8_t)(wn[r] >> (8 * k));
             }
           }
         }

@@ -28,6 +28,11 @@ int launch_2d_byte(bool is_signed, const void *in, int64_t batch, int64_t rows, 
                    void *out_min, int64_t out_ld, int64_t out_bstride, cudaStream_t s);
 // square windows the packed 1-byte kernel is compiled for (k2d_byte.cu)
 bool k2b_supports(int64_t w);
+// 1-byte grayscale opening / closing by a w x w square in three packed passes
+// (k2d_byte.cu); kErrUnsupported when the packed kernel does not apply
+int launch_morph_2d_byte(bool is_signed, const void *in, int64_t batch, int64_t rows, int64_t cols, int64_t in_ld,
+                         int64_t in_bstride, int64_t w, void *out_open, void *out_close, int64_t out_ld,
+                         int64_t out_bstride, void *e_buf, void *d_buf, int64_t buf_ld, cudaStream_t s);
 // LB_Keogh fused with the envelope (keogh.cu): float rows
 int launch_keogh(const float *c, int64_t batch, int64_t n, int64_t ld, const float *q, int64_t r, double *lb,
                  cudaStream_t s);

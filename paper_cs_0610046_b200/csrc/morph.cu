@@ -25,6 +25,9 @@
 // the interior of two padded buffers whose (w-1)-wide frames hold the
 // identities, then the 2-D max over the padded e and the 2-D min over the
 // padded d.  HBM: 1 read + 2 writes + 2 reads + 2 writes (vs 1 + 2 fused).
+// 1-byte pixels with the packed kernel's square windows skip the frames: the
+// second and third passes read e and ~d through the tensor map's zero frame
+// (launch_morph_2d_byte, k2d_byte.cu).
 #include "kwarp.cuh"
 #include "launch.cuh"
 
@@ -465,6 +468,14 @@ int launch_morph_2d(const void *in, int64_t batch, int64_t rows, int64_t cols, i
   if (batch == 0) return kOK;
   const Morph2DLayout<T> L(batch, rows, cols, w_row, w_col);
   char *base = static_cast<char *>(ws);
+  if constexpr (sizeof(T) == 1) {  // square windows of the packed kernel: three passes, no frames
+    if (w_row == w_col) {
+      const int rc = launch_morph_2d_byte(std::is_signed<T>::value, in, batch, rows, cols, in_ld, in_bstride, w_row,
+                                          out_open, out_close, out_ld, out_bstride, base + 2 * L.frame,
+                                          base + 2 * L.frame + L.valid, L.eld, s);
+      if (rc != kErrUnsupported) return rc;
+    }
+  }
   T *pe = reinterpret_cast<T *>(base);
   T *pd = reinterpret_cast<T *>(base + L.frame);
   {

@@ -195,3 +195,18 @@ def test_edge_values_3d(cuda_device, dtype):
     ex, en = oracle.separable_3d(vol, 5, 3, 4)
     same(mx, ex, "3d max")
     same(mn, en, "3d min")
+
+
+@pytest.mark.parametrize("dtype", [np.uint8, np.int8], ids=IDS)
+@pytest.mark.parametrize("w", [2, 5, 15, 17])
+def test_morph_2d_packed_framed_passes(cuda_device, dtype, w):
+    """1-byte square-window opening/closing (three packed passes, the second and
+    third reading through the tensor map's zero frame) on images spanning several
+    512-column strips and 498-row bands, against the oracle's composition."""
+    img = synth.c4(count=2, rows=1100, cols=1600, nrect=6)
+    if dtype == np.int8:
+        img = img.view(np.int8)
+    op, cl = mm.maxmin_morph_2d(torch.from_numpy(img).to(DEV), w, w)
+    eo, ec = oracle.morph_2d(img, w, w)
+    same(op, eo, f"open {w}x{w}")
+    same(cl, ec, f"close {w}x{w}")
