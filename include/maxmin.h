@@ -273,9 +273,14 @@ int maxmin_filter_2d_ws(int dt, const void *in, int64_t batch, int64_t rows, int
  * maxmin_morph_2d: images as maxmin_filter_2d; outputs [batch][rows][cols]
  *   with pitch out_ld / out_bstride, element alignment.  Device workspace of
  *   maxmin_morph_2d_workspace_bytes (two padded copies of the image: the
- *   erosion and the dilation framed by the identities).  Runs as the 2-D
- *   filter, then its max over the padded erosion and min over the padded
- *   dilation (the rectangle opening is not separable into 1-D openings).
+ *   erosion and the dilation framed by the identities, and two aligned
+ *   valid-region buffers).  Runs as the 2-D filter, then its max over the
+ *   padded erosion and min over the padded dilation (the rectangle opening is
+ *   not separable into 1-D openings).  1-byte pixels with square windows the
+ *   packed kernel takes (2..5, 7, 9, ..., 17; 16-B aligned input rows, 4-B
+ *   aligned output rows) run as three packed passes instead: erosion and
+ *   complemented dilation into the aligned buffers, then max filters of both
+ *   read through the tensor map's zero frame (no frame copies).
  */
 int maxmin_morph_batched(int dt, const void *in, int64_t batch, int64_t n, int64_t in_ld,
                          int64_t w, void *out_open, void *out_close, int64_t out_ld,

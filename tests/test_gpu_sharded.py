@@ -154,3 +154,34 @@ def test_sharded_argument_errors(cuda_device):
     assert e.value.status == 4
     with pytest.raises(ValueError):  # output sized for the last rank on a middle rank
         mm.maxmin_filter_1d_sharded(buf, 10_000, 100, [101], [torch.empty(9900, device=dev)], [None], 0, 2, None)
+
+
+def test_binding_checks_caller_outputs(cuda_device):
+    """The C ABI cannot see buffer sizes: the binding rejects outputs that are too
+    small, of another dtype or device, or whose strides differ between max and min."""
+    dev = torch.device("cuda:0")
+    x = torch.from_numpy(synth.c2(10_000)).to(dev)
+    m = 10_000 - 100 + 1
+    with pytest.raises(ValueError):
+        mm.maxmin_filter_1d(x, 100, out_max=torch.empty(m - 1, device=dev))
+    with pytest.raises(ValueError):
+        mm.maxmin_filter_1d(x, 100, out_max=torch.empty(m, dtype=torch.float64, device=dev))
+    with pytest.raises(ValueError):
+        mm.maxmin_filter_1d(x, 100, out_min=torch.empty(m))  # host tensor
+    rows = torch.from_numpy(synth.c3(rows=4, length=2000)).to(dev)
+    a = torch.empty(4, 2048, device=dev)[:, :1872]
+    b = torch.empty(4, 1888, device=dev)[:, :1872]
+    with pytest.raises(ValueError):
+        mm.maxmin_filter_batched(rows, 129, out_max=a, out_min=b)
+    # a supplied output with a wide pitch: the missing one is allocated with the same pitch
+    mx, mn = mm.maxmin_filter_batched(rows, 129, out_max=a)
+    assert mn.stride() == mx.stride() == a.stride()
+    ex, en = oracle.batched(rows.cpu().numpy(), 129)
+    assert np.array_equal(mx.cpu().numpy(), ex) and np.array_equal(mn.cpu().numpy(), en)
+    img = torch.from_numpy(synth.c4(count=1, rows=100, cols=160)).to(dev)
+    with pytest.raises(ValueError):
+        mm.maxmin_filter_2d(img, 5, 5, out_max=torch.empty(1, 95, 100, dtype=torch.uint8, device=dev))
+    host = torch.from_numpy(synth.c2(5000)).pin_memory()
+    ws = torch.empty(mm.maxmin_host_workspace_bytes(torch.float32, 5000, 33), dtype=torch.uint8, device=dev)
+    with pytest.raises(ValueError):
+        mm.maxmin_filter_1d_host(host, 33, torch.empty(100).pin_memory(), torch.empty(4968).pin_memory(), ws)
