@@ -330,7 +330,11 @@ __global__ void __launch_bounds__(NT, MM_LW_MINB) k1d_lw(Rows p, LwArgs g, void 
   auto publish = [&](const Pos &j, int fs, int ts) {
     if (!j.live) return;
     T gx, gn, hx, hn;
+#if MM_LW_ABL == 2  // ablation (wrong results): publish constants without reading the far chunk
+    if (false) {
+#else
     if (j.far) {
+#endif
       if (full_el < p.n) {
         patch_far(fs, j.row, (int64_t)j.x * WT + w - 1 - fsh, (Geo::NROWS + 1) * RW);
         __syncwarp();
@@ -470,7 +474,11 @@ __global__ void __launch_bounds__(NT, MM_LW_MINB) k1d_lw(Rows p, LwArgs g, void 
       const int e = lane + 32 * e2;
       if (e < nent) {
         uint64_t v = wv[e2];
+#if MM_LW_ABL == 1  // ablation (wrong results): never wait for a word
+        if ((v >> 32) == 0) v = pack_slot<T>(seed);
+#else
         if ((v >> 32) == 0) v = lw_wait(gb + (e2 == 0 ? eoff0 : e2 == 1 ? eoff1 : entry_off(e)), pst);
+#endif
         const T t = unpack_slot<T>(v);
         if (lane & 1)
           mn = Ord<T>::mn(mn, t);

@@ -726,3 +726,49 @@ def test_2d_plain_entry_generic_kernel(cuda_device, dtype):
             torch.cuda.synchronize()
             assert_same(ox, ex, f"{entry} max {wr}x{wc}")
             assert_same(on, en, f"{entry} min {wr}x{wc}")
+
+
+# ------------------------------------- round 2: SURVEY.md §4 items 2 and 3 ---
+
+@pytest.mark.parametrize("w", [3, 1024, 65536, 262144])
+def test_reversal_symmetry(cuda_device, w):
+    """F(rev a)[j] = F(a)[n-w-j] at C5's scale (no oracle): the large-window
+    kernel's front and the tile seams meet the data in the opposite order."""
+    a = synth.c5(1 << 24)
+    x = torch.from_numpy(a).to(dev())
+    mx, mn = mm.maxmin_filter_1d(x, w)
+    rx, rn = mm.maxmin_filter_1d(torch.flip(x, [0]).contiguous(), w)
+    assert torch.equal(torch.flip(rx, [0]), mx) and torch.equal(torch.flip(rn, [0]), mn)
+
+
+@pytest.mark.parametrize("dtype", [np.uint8, np.float32], ids=lambda d: np.dtype(d).name)
+@pytest.mark.parametrize("wr,wc", [(15, 15), (5, 11), (17, 3)])
+def test_2d_transpose_symmetry(cuda_device, dtype, wr, wc):
+    """F_{wr,wc}(A)^T = F_{wc,wr}(A^T) on 2 x 1200 x 1600 images."""
+    img = synth.c4(count=2, rows=1200, cols=1600, nrect=5)
+    if dtype == np.float32:
+        img = img.astype(np.float32)
+    x = torch.from_numpy(img).to(dev())
+    mx, mn = mm.maxmin_filter_2d(x, wr, wc)
+    xt = x.transpose(1, 2).contiguous()
+    tx, tn = mm.maxmin_filter_2d(xt, wc, wr)
+    assert torch.equal(mx.transpose(1, 2), tx) and torch.equal(mn.transpose(1, 2), tn)
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 37, 64, 129])
+def test_batched_many_tiny_problems(cuda_device, n):
+    """Thousands of tiny random problems in one launch (the batched API), every w,
+    against the brute-force definition; tie-heavy values."""
+    rows = 4096
+    a = synth.random_values(np.int32, rows * n, seed=100 + n, alphabet=8).reshape(rows, n)
+    ld = (n + 3) // 4 * 4
+    buf = np.zeros((rows, ld), np.int32)
+    buf[:, :n] = a
+    x = torch.from_numpy(buf).to(dev())
+    for w in sorted({1, 2, 3, n // 2 + 1, n}):
+        if w > n or w < 1:
+            continue
+        mx, mn = mm.maxmin_filter_batched(x, w, n=n)
+        win = np.lib.stride_tricks.sliding_window_view(a, w, axis=1)
+        assert np.array_equal(mx.cpu().numpy(), win.max(axis=2)), (n, w)
+        assert np.array_equal(mn.cpu().numpy(), win.min(axis=2)), (n, w)
