@@ -6,6 +6,7 @@
   image against the oracle's separable filter.
 * C5 in full: all 2^30 - w + 1 windows for w in {7, 4096, 262144}, compared in
   chunks against the oracle's appendix listing (chunks filtered on host threads).
+* C3 in full: all 65536 series of 4096 samples, w=129, in one batched call.
 * Edge values (synth.edge_values): dtype extremes, +-inf, subnormals, long equal
   runs, through every kernel family: 1-D small / medium / large-window paths,
   batched rows, the 2-D packed-byte, separable and generic kernels, the arg
@@ -61,6 +62,27 @@ def test_c4_full_size_every_image(cuda_device):
         ex, en = oracle.separable_2d(host[b], w, w)
         same(ox[b, :, :Co], ex, f"C4 image {b} max")
         same(on[b, :, :Co], en, f"C4 image {b} min")
+
+
+@pytest.mark.slow
+def test_c3_full_size_every_row(cuda_device):
+    """BASELINE config C3 in full: 65536 series x 4096, w=129, one batched call (the
+    bench's), every row against the oracle (row blocks on host threads)."""
+    B, n, w = synth.C3["batch"], synth.C3["n"], synth.C3["w"]
+    host = synth.c3()
+    x = torch.from_numpy(host).to(DEV)
+    mx, mn = mm.maxmin_filter_batched(x, w)
+    gx, gn = mx.cpu().numpy(), mn.cpu().numpy()
+    del x, mx, mn
+    blocks = [(r, min(r + 4096, B)) for r in range(0, B, 4096)]
+
+    def one(b):
+        return b, oracle.batched(host[b[0]:b[1]], w)
+
+    with cf.ThreadPoolExecutor(max_workers=8) as pool:
+        for (r0, r1), (ex, en) in pool.map(one, blocks):
+            same(gx[r0:r1], ex, f"C3 rows {r0}..{r1} max")
+            same(gn[r0:r1], en, f"C3 rows {r0}..{r1} min")
 
 
 def _chunked_compare(a, w, gx, gn, chunk=1 << 25, threads=8):
