@@ -141,15 +141,18 @@ class ClockSampler:
                 "window": "soak steps right before the timed region + the timed region"}
 
 
-def timed_loop(step, steps: int, stream, clk: ClockSampler, soak_s: float = 0.25):
-    """Untimed soak (>= soak_s of steps, for the clock record) then EXACTLY `steps`
-    steps between two CUDA events on `stream`.  Returns ms."""
+def timed_loop(step, steps: int, stream, clk: ClockSampler, soak_s: float = 0.25, soak_steps: int | None = None):
+    """Untimed soak (>= soak_s of steps, or exactly soak_steps -- multi-rank runs,
+    whose steps must pair up across ranks), for the clock record, then EXACTLY
+    `steps` steps between two CUDA events on `stream`.  Returns ms."""
     import torch
 
     t_soak = time.perf_counter()
-    while time.perf_counter() - t_soak < soak_s:
+    k = 0
+    while (time.perf_counter() - t_soak < soak_s) if soak_steps is None else (k < soak_steps):
         step()
         torch.cuda.synchronize()
+        k += 1
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -423,9 +426,15 @@ def run_1d(args, rank, world, local):
 
     clk = ClockSampler(local)
     with clk:
+        t_w = time.perf_counter()
         for _ in range(args.warmup):
             step()
         barrier()
+        soak_steps = None
+        if world > 1:  # the same soak length on every rank (NCCL sends and receives pair up)
+            per = torch.tensor([(time.perf_counter() - t_w) / max(args.warmup, 1)], dtype=torch.float64, device=dev)
+            dist.all_reduce(per, op=dist.ReduceOp.MAX)
+            soak_steps = int(min(1000, max(3, 0.25 / max(float(per.item()), 1e-6))))
         # bit-exact check of this run's outputs against the oracle (untimed):
         # slices around tile seams, and at N > 1 every window of the rank seam
         parity = spot_check(glob_np, c0, n_local, last, outs, windows)
@@ -440,7 +449,7 @@ def run_1d(args, rank, world, local):
         barrier()
         if world == 1:
             record["on"] = True
-        ms = timed_loop(step, args.steps, stream, clk)
+        ms = timed_loop(step, args.steps, stream, clk, soak_steps=soak_steps)
         record["on"] = False
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
