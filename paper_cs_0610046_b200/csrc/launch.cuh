@@ -411,7 +411,7 @@ template <typename T>
 static int launch_warp(const Rows &p, void *ws, size_t ws_bytes, cudaStream_t s) {
   if constexpr (sizeof(T) > 4) {
     return kErrUnsupported;
-  } else if (MM_LW) {
+  } else if constexpr (MM_LW) {
     return launch_lw<T>(p, ws, ws_bytes, s);
   } else {
     using Geo = WarpGeo<T>;
