@@ -2,7 +2,7 @@
 # default bench, ncu --set full captures behind each config (summaries into
 # gpurun_out/profiles_new/round2 + the traffic table).
 cd $GRAFT_REPO_ROOT
-D=gpurun_out/ev2
+D=gpurun_out/${EVD:-ev2}
 mkdir -p $D
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem,power.draw --format=csv > $D/smi.txt 2>&1
 timeout 900 python bench.py > $D/bench_C2.log 2>&1; echo "rc=$?" >> $D/bench_C2.log
