@@ -95,9 +95,9 @@ size_t maxmin_dtype_size(int dt);
 /*
  * Workspace needed by maxmin_filter_1d / maxmin_filter_batched for these
  * arguments, written to *bytes.  It is 0 unless the cross-CTA look-back path
- * runs (w - 1 >= 512 for <= 4-byte types, DESIGN.md kernel "k1d_lw": a ticket
- * counter + 256 B per 4096 windows of every row; w - 1 > 8192 for 8-byte
- * types, kernel "large": ~32 B per 2048 windows).  The library zeroes what it
+ * runs (w > 8193; <= 4-byte types: DESIGN.md kernel "k1d_lw", a ticket
+ * counter + 256 B per 4096 windows of every row; 8-byte types: kernel
+ * "large", ~32 B per 2048 windows).  The library zeroes what it
  * needs of it on `stream` at every call.
  */
 int maxmin_workspace_bytes(int dt, int64_t batch, int64_t n, int64_t w,
