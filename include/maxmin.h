@@ -159,7 +159,9 @@ int maxmin_filter_2d(int dt, const void *in, int64_t batch, int64_t rows,
  *   Any of the four outputs may be NULL (at least one must not be); all four
  *   use the row pitch out_ld (elements).  Value outputs need element
  *   alignment, position outputs (int64) 8-byte alignment; in needs element
- *   alignment.  dtypes of <= 4 bytes (else MAXMIN_ERR_UNSUPPORTED) and
+ *   alignment.  The vector load/store paths need 16-byte base pointers and,
+ *   when batch > 1, 16-byte pitches; other layouts take element-wise paths
+ *   (same results, slower).  dtypes of <= 4 bytes (else MAXMIN_ERR_UNSUPPORTED) and
  *   n < 2^32.  Workspace: maxmin_argfilter_workspace_bytes (~32 bytes per
  *   element: the 64-bit (value, position) keys and their filtered copies).
  *   Runs as keys -> max/min filters on the keys -> decode, all on the device.
@@ -268,7 +270,8 @@ int maxmin_filter_2d_ws(int dt, const void *in, int64_t batch, int64_t rows, int
  *
  * maxmin_morph_batched: rows b of in + b*in_ld (n samples each); out_open /
  *   out_close (either may be NULL) rows at pitch out_ld, 16-byte aligned with
- *   16-byte row pitch; in needs element alignment.  w - 1 <= 8192 (else
+ *   a 16-byte row pitch when batch > 1 (one row: any pitch, it never enters an
+ *   address); in needs element alignment.  w - 1 <= 8192 (else
  *   MAXMIN_ERR_UNSUPPORTED; 8-byte types stop where a warp's staging no longer
  *   fits shared memory, about w - 1 <= 4000).  One fused kernel: the input is read once and
  *   each output written once.  No workspace.

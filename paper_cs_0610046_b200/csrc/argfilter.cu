@@ -491,8 +491,9 @@ int launch_arg_medium(const void *in, int64_t batch, int64_t n, int64_t in_ld, i
   epi.arg_min = arg_min;
   epi.out_ld = out_ld;
   auto al = [](const void *q) { return q == nullptr || reinterpret_cast<uintptr_t>(q) % 16 == 0; };
-  epi.vec = (al(out_max) && al(out_min) && al(arg_max) && al(arg_min) && (out_ld * 8) % 16 == 0 &&
-             (out_ld * (int64_t)sizeof(S)) % 16 == 0) ? 1 : 0;
+  // one row: the pitch never enters an address, so only the base pointers matter
+  epi.vec = (al(out_max) && al(out_min) && al(arg_max) && al(arg_min) &&
+             (batch == 1 || ((out_ld * 8) % 16 == 0 && (out_ld * (int64_t)sizeof(S)) % 16 == 0))) ? 1 : 0;
   switch (medium_G<uint64_t>(w)) {
     case 1: return launch_arg_medium_g<S, 1>(p, maps, epi, s);
     case 2: return launch_arg_medium_g<S, 2>(p, maps, epi, s);
@@ -526,10 +527,11 @@ int launch_arg_fused(const void *in, int64_t batch, int64_t n, int64_t in_ld, in
   a.nseg = batch * a.segs_per_row;
   if (a.nseg > 0x7fffffffLL) return kErrUnsupported;
   a.w = (int)w;
-  a.in_vec = (reinterpret_cast<uintptr_t>(in) % 16 == 0 && (in_ld * (int64_t)sizeof(S)) % 16 == 0) ? 1 : 0;
+  a.in_vec = (reinterpret_cast<uintptr_t>(in) % 16 == 0 && (batch == 1 || (in_ld * (int64_t)sizeof(S)) % 16 == 0))
+                 ? 1 : 0;
   auto al = [](const void *p) { return p == nullptr || reinterpret_cast<uintptr_t>(p) % 16 == 0; };
-  a.out_vec = (al(out_max) && al(out_min) && al(arg_max) && al(arg_min) && (out_ld * 8) % 16 == 0 &&
-               (out_ld * (int64_t)sizeof(S)) % 16 == 0) ? 1 : 0;
+  a.out_vec = (al(out_max) && al(out_min) && al(arg_max) && al(arg_min) &&
+               (batch == 1 || ((out_ld * 8) % 16 == 0 && (out_ld * (int64_t)sizeof(S)) % 16 == 0))) ? 1 : 0;
   if (w - 1 < E) {
     a.g.w = (int)w;
     return launch_arg_g<S, 0>(a, s);

@@ -310,7 +310,8 @@ int launch_morph(const void *in, int64_t batch, int64_t n, int64_t in_ld, int64_
   a.nseg = batch * a.segs_per_row;
   if (a.nseg > 0x7fffffffLL) return kErrUnsupported;
   a.w = (int)w;
-  a.in_vec = (reinterpret_cast<uintptr_t>(in) % 16 == 0 && (in_ld * (int64_t)sizeof(T)) % 16 == 0) ? 1 : 0;
+  a.in_vec = (reinterpret_cast<uintptr_t>(in) % 16 == 0 && (batch == 1 || (in_ld * (int64_t)sizeof(T)) % 16 == 0))
+                 ? 1 : 0;
   a.stage_bytes = Geo::stage_bytes((int)w);
   a.ebuf_bytes = Geo::ebuf_bytes((int)w);
   if (w - 1 < Geo::E) {

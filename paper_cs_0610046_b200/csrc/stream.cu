@@ -340,7 +340,8 @@ int launch_stream_push(void *state, const StreamLayout &L, int64_t streams, int6
     a.streams = streams;
     a.w = (int)w;
     a.P = (int)(L.ld - h);
-    a.chunk_vec = (reinterpret_cast<uintptr_t>(chunk) % 16 == 0 && (chunk_ld * (int64_t)sizeof(T)) % 16 == 0) ? 1 : 0;
+    a.chunk_vec = (reinterpret_cast<uintptr_t>(chunk) % 16 == 0 &&
+                   (streams == 1 || (chunk_ld * (int64_t)sizeof(T)) % 16 == 0)) ? 1 : 0;
     if (h < EB) {  // w <= E: the small-window path
       if (ES < EB && c <= 32 * ES && h < ES) return launch_fused_g<T, ES, 0>(a, s);
       return launch_fused_g<T, EB, 0>(a, s);

@@ -400,6 +400,43 @@ def test_argfilter_unaligned_rows_and_outputs(cuda_device):
         assert_same(an[sl], ean, f"row {r} argmin")
 
 
+@pytest.mark.parametrize("w", [5, 129, 1024])
+def test_single_row_pitch_is_free(cuda_device, w):
+    """One row through the C ABI with the natural pitches (in_ld = n, out_ld = m, both
+    odd): a pitch never enters an address when batch == 1, so the vector paths run
+    (the bench's N1 call) and the results match the oracle."""
+    import ctypes
+
+    n = 40_001
+    m = n - w + 1
+    a = synth.random_values(np.float32, n, seed=90 + w, alphabet=7)
+    x = torch.from_numpy(a).to(dev())
+    L = mm._lib.lib()
+    vp = ctypes.c_void_p
+    s = vp(torch.cuda.current_stream().cuda_stream)
+    code = mm.dtype_code(torch.float32)
+    ox, on = torch.empty(m, device=dev()), torch.empty(m, device=dev())
+    ax = torch.empty(m, dtype=torch.int64, device=dev())
+    an = torch.empty_like(ax)
+    need = mm.maxmin_argfilter_workspace_bytes(torch.float32, 1, n, w)
+    ws = torch.empty(max(need, 16), dtype=torch.uint8, device=dev())
+    mm._lib.check(L.maxmin_argfilter_batched(code, vp(x.data_ptr()), 1, n, n, w, vp(ox.data_ptr()),
+                                             vp(on.data_ptr()), vp(ax.data_ptr()), vp(an.data_ptr()), m,
+                                             vp(ws.data_ptr()), ws.numel(), s))
+    op, cl = torch.empty(n, device=dev()), torch.empty(n, device=dev())
+    mm._lib.check(L.maxmin_morph_batched(code, vp(x.data_ptr()), 1, n, n, w, vp(op.data_ptr()),
+                                         vp(cl.data_ptr()), n, s))
+    torch.cuda.synchronize()
+    ex, en, eax, ean = oracle.arg_wedge(a, w)
+    assert_same(ox, ex, "arg values max")
+    assert_same(on, en, "arg values min")
+    assert_same(ax, eax, "argmax")
+    assert_same(an, ean, "argmin")
+    eo, ec = oracle.morph(a, w)
+    assert_same(op, eo, "opening")
+    assert_same(cl, ec, "closing")
+
+
 def test_argfilter_c2_full_size(cuda_device):
     """C2's array (n = 2^28) at w = 1024: positions vs the wedge oracle."""
     a = synth.c2(1 << 28)
