@@ -139,6 +139,9 @@ __device__ __forceinline__ uint64_t lw_wait(const uint64_t *s, LwStats &st) {
 #endif
 }
 
+#ifndef MM_LW_NW0  // gap words per lane loaded before the scans (nent <= 32*NW0; 4: q <= 504)
+#define MM_LW_NW0 4
+#endif
 #ifndef MM_LW_MINB  // resident CTAs per SM the register budget is sized for
 #define MM_LW_MINB 2
 #endif
@@ -397,7 +400,7 @@ __global__ void __launch_bounds__(NT, MM_LW_MINB) k1d_lw(Rows p, LwArgs g, void 
     const int64_t u0 = (int64_t)j.x * WT;
     // gap words first: their latency overlaps the scans
     const uint64_t *gb = gw + (int64_t)j.tk * 32;
-    constexpr int NW0 = 4;  // words per lane held in flight (nent <= 128: q <= 504)
+    constexpr int NW0 = MM_LW_NW0;  // words per lane held in flight (nent <= 32*NW0)
     uint64_t wv[NW0];
 #pragma unroll
     for (int e2 = 0; e2 < NW0; ++e2) {
@@ -486,7 +489,7 @@ __global__ void __launch_bounds__(NT, MM_LW_MINB) k1d_lw(Rows p, LwArgs g, void 
           mx = Ord<T>::mx(mx, t);
       }
     }
-    for (int e = lane + 32 * NW0; e < nent; e += 32) {  // very large windows (q > 504)
+    for (int e = lane + 32 * NW0; e < nent; e += 32) {  // very large windows (nent > 32*NW0)
       const T t = unpack_slot<T>(lw_wait(gb + entry_off(e), pst));
       if (lane & 1)
         mn = Ord<T>::mn(mn, t);
