@@ -318,6 +318,8 @@ def main(argv=None):
 
     if args.spawn_check:
         return spawn_check(rank, world, local)
+    if local >= torch.cuda.device_count():  # one GPU per rank, never two ranks on one GPU
+        sys.exit(f"bench.py: rank {rank} needs GPU {local} but {torch.cuda.device_count()} are visible")
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
