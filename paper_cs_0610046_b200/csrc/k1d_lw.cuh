@@ -110,9 +110,6 @@ __device__ __forceinline__ uint32_t atom_add_shared(uint32_t *p, uint32_t v) {
   asm volatile("atom.shared.acq_rel.cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
   return old;
 }
-__device__ __forceinline__ void mbar_arrive1(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 // wait_slot with optional per-lane counters (polled words, spin iterations,
 // cycles), added to the workspace header once per warp at the end

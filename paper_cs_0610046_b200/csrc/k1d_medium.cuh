@@ -115,6 +115,16 @@ struct MedLayoutS {
   }
 };
 
+// MM_MED_SPLIT: the per-tile CTA barrier split into mbarrier hand-offs -- the
+// ring is "ready" once every warp has published its far-block aggregates (one
+// arrival per warp right after the far chunk, waited on just before the gap,
+// so the near-chunk scan runs in between), and a stage is "empty" once every
+// warp has consumed its loads (only the producer thread waits, before the next
+// prefetch into it).
+#ifndef MM_MED_SPLIT
+#define MM_MED_SPLIT 0
+#endif
+
 template <typename T, int G, class Epi = StoreEpi, class Src = SameSrc<T>>
 __global__ void __launch_bounds__(NT, 2)
     k1d_medium(Rows p, MedGeom g, const __grid_constant__ TmaMaps maps, Epi epi = Epi()) {
@@ -159,6 +169,11 @@ __global__ void __launch_bounds__(NT, 2)
     prefetch_tmap(&maps.small);
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
+#if MM_MED_SPLIT
+    mbar_init(&bars[2], NT / 32);  // stage 0 empty
+    mbar_init(&bars[3], NT / 32);  // stage 1 empty
+    mbar_init(&bars[4], NT / 32);  // ring ready
+#endif
     fence_mbar_init();
   }
   __syncthreads();
@@ -186,8 +201,12 @@ __global__ void __launch_bounds__(NT, 2)
     const int st = it & 1;
     const unsigned char *X = stg(st);
     nxt.advance(p);
-    if (tid == 0 && t + 1 < t_end)  // prefetch the next tile into the other stage
+    if (tid == 0 && t + 1 < t_end) {  // prefetch the next tile into the other stage
+#if MM_MED_SPLIT
+      if (it > 0) mbar_wait(&bars[2 + (st ^ 1)], ((it - 1) >> 1) & 1);  // tile it-1 consumed it
+#endif
       stage_tile2<S>(p, &maps, stg(st ^ 1), nxt.row, nxt.u0, nxt.tout(p) + w - 1, &bars[st ^ 1]);
+    }
     const int64_t row = cur.row, u0 = cur.u0;
     const int tout = cur.tout(p);
     const int64_t ab0 = u0 / B;  // far block index (within the row) of group 0
@@ -231,6 +250,47 @@ __global__ void __launch_bounds__(NT, 2)
       }
     }
 
+    // ---------------- far blocks before the tile (first tiles of a range/row)
+    auto far_blocks_before = [&]() {
+      const int64_t tile_in_row = u0 / TILE;
+      if (g.V > 0 && (t - t_begin < g.need || tile_in_row < g.need)) {
+        const int nv = g.V * G;  // chunks of the V blocks
+        for (int r0 = 0; r0 < nv; r0 += NT) {
+          const int vc = r0 + tid;
+          if (r0 + (tid & ~31) >= nv) break;  // whole warp idle (warp-uniform)
+          const int vcc = vc < nv ? vc : nv - 1;
+          const int gv = vcc / G;  // 0 .. V-1  <->  g' = gv - V
+          const int pos = (gv - g.V) * B + w - 1 + gl * E;
+          T ya[E], yb[E];
+          Src::template load<E>(X, pos, u0, ya, yb);
+          T ax = ya[0], an = yb[0];
+#pragma unroll
+          for (int k = 1; k < E; ++k) {
+            ax = Ord<T>::mx(ax, ya[k]);
+            an = Ord<T>::mn(an, yb[k]);
+          }
+          T hx, hn, tx, tn;
+          h_part(ya, ax, an, __shfl_sync(0xffffffffu, ya[E - 1], glast), hx, tn);
+          if (TWO) h_part(yb, ax, an, __shfl_sync(0xffffffffu, yb[E - 1], glast), tx, hn);
+          else hn = tn;
+          grp_reduce<T, G>(ax, an);
+          grp_reduce<T, G>(hx, hn);
+          if (vc < nv && gl == 0) {
+            const int ri = (int)((ab0 + gv - g.V) & RMASK);
+            Rgx[ri] = ax;
+            Rgn[ri] = an;
+            Rhx[ri] = hx;
+            Rhn[ri] = hn;
+          }
+        }
+      }
+    };
+#if MM_MED_SPLIT
+    far_blocks_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive1(&bars[4]);  // this warp's ring entries are written
+#endif
+
     // ------------------------------------------------ near chunk: suffix
     {
       T xa[E], xb[E];
@@ -256,40 +316,14 @@ __global__ void __launch_bounds__(NT, 2)
       cn = Ord<T>::mn(cn, en);
     }
 
-    // ---------------- far blocks before the tile (first tiles of a range/row)
-    const int64_t tile_in_row = u0 / TILE;
-    if (g.V > 0 && (t - t_begin < g.need || tile_in_row < g.need)) {
-      const int nv = g.V * G;  // chunks of the V blocks
-      for (int r0 = 0; r0 < nv; r0 += NT) {
-        const int vc = r0 + tid;
-        if (r0 + (tid & ~31) >= nv) break;  // whole warp idle (warp-uniform)
-        const int vcc = vc < nv ? vc : nv - 1;
-        const int gv = vcc / G;  // 0 .. V-1  <->  g' = gv - V
-        const int pos = (gv - g.V) * B + w - 1 + gl * E;
-        T ya[E], yb[E];
-        Src::template load<E>(X, pos, u0, ya, yb);
-        T ax = ya[0], an = yb[0];
-#pragma unroll
-        for (int k = 1; k < E; ++k) {
-          ax = Ord<T>::mx(ax, ya[k]);
-          an = Ord<T>::mn(an, yb[k]);
-        }
-        T hx, hn, tx, tn;
-        h_part(ya, ax, an, __shfl_sync(0xffffffffu, ya[E - 1], glast), hx, tn);
-        if (TWO) h_part(yb, ax, an, __shfl_sync(0xffffffffu, yb[E - 1], glast), tx, hn);
-        else hn = tn;
-        grp_reduce<T, G>(ax, an);
-        grp_reduce<T, G>(hx, hn);
-        if (vc < nv && gl == 0) {
-          const int ri = (int)((ab0 + gv - g.V) & RMASK);
-          Rgx[ri] = ax;
-          Rgn[ri] = an;
-          Rhx[ri] = hx;
-          Rhn[ri] = hn;
-        }
-      }
-    }
+#if MM_MED_SPLIT
+    __syncwarp();
+    if (lane == 0) mbar_arrive1(&bars[2 + st]);  // this warp is done with the stage
+    mbar_wait(&bars[4], it & 1);                 // every warp's ring entries of this tile
+#else
+    far_blocks_before();
     __syncthreads();
+#endif
 
     // ---------------------------------------------------------- gap + out
     if (g.qp > 0 || g.rp > 0) {
