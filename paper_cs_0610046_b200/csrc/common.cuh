@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #ifndef __CUDACC__
@@ -247,6 +248,28 @@ template <>
 __device__ __forceinline__ uint16_t shfl_down(uint16_t v, int d) { return (uint16_t)__shfl_down_sync(0xffffffffu, (uint32_t)v, d); }
 template <>
 __device__ __forceinline__ int16_t shfl_down(int16_t v, int d) { return (int16_t)__shfl_down_sync(0xffffffffu, (int32_t)v, d); }
+
+// Segmented shuffles (aligned segments of `width` lanes): a lane whose source
+// lies outside its segment gets its own value back, so an idempotent scan step
+// (max/min) needs no lane predicate: v = op(v, shfl_up_seg(v, d, width)).
+template <typename T>
+__device__ __forceinline__ T shfl_up_seg(T v, int d, int width) {
+  if constexpr (sizeof(T) < 4) {
+    using W = typename std::conditional<std::is_signed<T>::value, int32_t, uint32_t>::type;
+    return (T)__shfl_up_sync(0xffffffffu, (W)v, d, width);
+  } else {
+    return __shfl_up_sync(0xffffffffu, v, d, width);
+  }
+}
+template <typename T>
+__device__ __forceinline__ T shfl_down_seg(T v, int d, int width) {
+  if constexpr (sizeof(T) < 4) {
+    using W = typename std::conditional<std::is_signed<T>::value, int32_t, uint32_t>::type;
+    return (T)__shfl_down_sync(0xffffffffu, (W)v, d, width);
+  } else {
+    return __shfl_down_sync(0xffffffffu, v, d, width);
+  }
+}
 
 // --------------------------------------------------- release / acquire ------
 __device__ __forceinline__ void st_release_u32(uint32_t *p, uint32_t v) {

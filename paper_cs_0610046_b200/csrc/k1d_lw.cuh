@@ -422,11 +422,8 @@ __global__ void __launch_bounds__(NT, MM_LW_MINB) k1d_lw(Rows p, LwArgs g, void 
     T cx = px[E - 1], cn = pn[E - 1];
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      const T vx = shfl_up(cx, d), vn = shfl_up(cn, d);
-      if (lane >= d) {
-        cx = Ord<T>::mx(cx, vx);
-        cn = Ord<T>::mn(cn, vn);
-      }
+      cx = Ord<T>::mx(cx, shfl_up(cx, d));  // (lanes below d get their own value: idempotent)
+      cn = Ord<T>::mn(cn, shfl_up(cn, d));
     }
     T Cx = shfl_up(cx, 1), Cn = shfl_up(cn, 1);  // exclusive carries (lane 0: the seed)
     if (lane == 0) Cx = Cn = seed;
@@ -444,11 +441,8 @@ __global__ void __launch_bounds__(NT, MM_LW_MINB) k1d_lw(Rows p, LwArgs g, void 
       T bx = sx[0], bn = sn[0];
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
-        const T vx = shfl_down(bx, d), vn = shfl_down(bn, d);
-        if (lane + d < 32) {
-          bx = Ord<T>::mx(bx, vx);
-          bn = Ord<T>::mn(bn, vn);
-        }
+        bx = Ord<T>::mx(bx, shfl_down(bx, d));
+        bn = Ord<T>::mn(bn, shfl_down(bn, d));
       }
       T ex = shfl_down(bx, 1), en = shfl_down(bn, 1);
       if (lane == 31) ex = en = seed;

@@ -58,22 +58,18 @@ template <typename T, int G>
 __device__ __forceinline__ void grp_scan_up(T &vx, T &vn, int gl) {
 #pragma unroll
   for (int d = 1; d < G; d <<= 1) {
-    const T ux = shfl_up(vx, d), un = shfl_up(vn, d);
-    if (gl >= d) {
-      vx = Ord<T>::mx(vx, ux);
-      vn = Ord<T>::mn(vn, un);
-    }
+    (void)gl;  // lanes below d of their group get their own value back (idempotent step)
+    vx = Ord<T>::mx(vx, shfl_up_seg(vx, d, G));
+    vn = Ord<T>::mn(vn, shfl_up_seg(vn, d, G));
   }
 }
 template <typename T, int G>
 __device__ __forceinline__ void grp_scan_down(T &vx, T &vn, int gl) {
 #pragma unroll
   for (int d = 1; d < G; d <<= 1) {
-    const T ux = shfl_down(vx, d), un = shfl_down(vn, d);
-    if (gl + d < G) {
-      vx = Ord<T>::mx(vx, ux);
-      vn = Ord<T>::mn(vn, un);
-    }
+    (void)gl;
+    vx = Ord<T>::mx(vx, shfl_down_seg(vx, d, G));
+    vn = Ord<T>::mn(vn, shfl_down_seg(vn, d, G));
   }
 }
 

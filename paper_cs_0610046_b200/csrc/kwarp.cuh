@@ -357,8 +357,7 @@ __device__ __forceinline__ void warp_window_med1(const unsigned char *X, int pos
     T a = u[E - 1];
 #pragma unroll
     for (int d = 1; d < G; d <<= 1) {
-      const T t = shfl_up(a, d);
-      if (gl >= d) a = op1<T, MAX>(a, t);
+      a = op1<T, MAX>(a, shfl_up_seg(a, d, G));  // (own value below d: idempotent)
     }
     c = shfl_up(a, 1);
     if (gl == 0) c = y[0];
@@ -380,8 +379,7 @@ __device__ __forceinline__ void warp_window_med1(const unsigned char *X, int pos
     T b = sfx;
 #pragma unroll
     for (int d = 1; d < G; d <<= 1) {
-      const T t = shfl_down(b, d);
-      if (gl + d < G) b = op1<T, MAX>(b, t);
+      b = op1<T, MAX>(b, shfl_down_seg(b, d, G));
     }
     T e = shfl_down(b, 1);
     if (gl == G - 1) e = x[E - 1];
