@@ -143,6 +143,13 @@ __device__ __forceinline__ void st_cs_16(void *p, uint4 v) {
                : "memory");
 }
 
+// shared-memory atomic add, acquire-release at CTA scope (hand-offs by election)
+__device__ __forceinline__ uint32_t atom_add_shared_u32(uint32_t *p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.acq_rel.cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+  return old;
+}
+
 // 32-byte store (sm_100: STG.E.256): one whole L2 sector per lane, so a warp
 // store of lane-strided chunks writes only full sectors.
 __device__ __forceinline__ void st_cs_32(void *p, const uint32_t (&r)[8]) {

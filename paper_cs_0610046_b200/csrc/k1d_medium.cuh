@@ -40,8 +40,8 @@ struct MedLayout {
     return (r + kBoxRows - 1) / kBoxRows * kBoxRows;
   }
   __host__ __device__ static size_t stage_bytes(int64_t w) { return (size_t)rows(w) * 128; }
-  __host__ __device__ static size_t bytes(int64_t w, int ring) {
-    return 1024 + 2 * stage_bytes(w) + 4 * sizeof(T) * (size_t)ring + 64;
+  __host__ __device__ static size_t bytes(int64_t w, int ring, int nstg = 2) {
+    return 1024 + nstg * stage_bytes(w) + 4 * sizeof(T) * (size_t)ring + 64;
   }
 };
 
@@ -106,8 +106,8 @@ struct MedLayoutS {
     return (r + kBoxRows - 1) / kBoxRows * kBoxRows;
   }
   __host__ __device__ static size_t stage_bytes(int64_t w) { return (size_t)rows(w) * 128; }
-  __host__ __device__ static size_t bytes(int64_t w, int ring) {
-    return 1024 + 2 * stage_bytes(w) + 4 * sizeof(T) * (size_t)ring + 64;
+  __host__ __device__ static size_t bytes(int64_t w, int ring, int nstg = 2) {
+    return 1024 + nstg * stage_bytes(w) + 4 * sizeof(T) * (size_t)ring + 64;
   }
 };
 
@@ -121,7 +121,18 @@ struct MedLayoutS {
 #define MM_MED_SPLIT 0
 #endif
 
-template <typename T, int G, class Epi = StoreEpi, class Src = SameSrc<T>>
+// DIRECT (q' = 0, i.e. w-1 < 2B: every w <= 32E+1): the gap of group g is
+// only H_{g-1}, the last r' elements of F_{g-1} = [gB-B+w-1, gB+w-1), and the
+// tile's stage holds F_{g-1} (w-1 >= B).  So the group reduces it itself from
+// the stage instead of reading the aggregate its predecessor published: no
+// ring, no cross-warp dependency and no per-tile CTA barrier.  Three stages;
+// a stage is recycled once every warp has arrived on its "empty" mbarrier.
+template <int DIRECT>
+struct MedStages {
+  static constexpr int N = DIRECT ? 3 : 2;
+};
+
+template <typename T, int G, class Epi = StoreEpi, class Src = SameSrc<T>, bool DIRECT = false>
 __global__ void __launch_bounds__(NT, 2)
     k1d_medium(Rows p, MedGeom g, const __grid_constant__ TmaMaps maps, Epi epi = Epi()) {
   using Lay = MedLayout<T>;
@@ -139,11 +150,12 @@ __global__ void __launch_bounds__(NT, 2)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *base = smem_align1024(smem_raw);
   auto stg = [&](int i) { return base + i * SB; };
-  T *Rgx = reinterpret_cast<T *>(base + 2 * SB);  // ring of far-block aggregates
+  constexpr int NSTG = MedStages<DIRECT>::N;
+  T *Rgx = reinterpret_cast<T *>(base + NSTG * SB);  // ring of far-block aggregates (unused if DIRECT)
   T *Rgn = Rgx + g.ring;
   T *Rhx = Rgn + g.ring;
   T *Rhn = Rhx + g.ring;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(base + 2 * SB + 4 * sizeof(T) * g.ring);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(base + NSTG * SB + 4 * sizeof(T) * g.ring);
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -165,6 +177,10 @@ __global__ void __launch_bounds__(NT, 2)
     prefetch_tmap(&maps.small);
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
+    if (DIRECT) {
+      mbar_init(&bars[2], 1);  // stage 2 full
+      for (int i = 0; i < NSTG; ++i) reinterpret_cast<uint32_t *>(bars + NSTG)[i] = 0;  // stage i: warps done
+    }
 #if MM_MED_SPLIT
     mbar_init(&bars[2], NT / 32);  // stage 0 empty
     mbar_init(&bars[3], NT / 32);  // stage 1 empty
@@ -173,8 +189,19 @@ __global__ void __launch_bounds__(NT, 2)
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0 && t_begin < t_end)
+  TileCursor<TILE> pf = cur;  // DIRECT: tile it+NSTG during tile it
+  uint32_t *done = reinterpret_cast<uint32_t *>(bars + NSTG);  // DIRECT: per stage, warps done with it
+  if (tid == 0 && t_begin < t_end) {
     stage_tile2<S>(p, &maps, stg(0), cur.row, cur.u0, cur.tout(p) + w - 1, &bars[0]);
+    for (int k = 1; DIRECT && k < NSTG; ++k) {
+      pf.advance(p);
+      if (t_begin + k < t_end) stage_tile2<S>(p, &maps, stg(k), pf.row, pf.u0, pf.tout(p) + w - 1, &bars[k]);
+    }
+  }
+  if (DIRECT) {
+    pf = cur;
+    for (int k = 0; k < NSTG; ++k) pf.advance(p);
+  }
 
   // H contribution of a chunk y (block-relative chunk gl) given its local max
   auto h_part = [&](const T (&y)[E], T ax, T an, T bl, T &hx, T &hn) {
@@ -192,12 +219,13 @@ __global__ void __launch_bounds__(NT, 2)
     }
   };
 
-  int it = 0;
-  for (int64_t t = t_begin; t < t_end; ++t, ++it) {
-    const int st = it & 1;
+  int it = 0, st = 0;
+  for (int64_t t = t_begin; t < t_end; ++t, ++it, st = st + 1 == NSTG ? 0 : st + 1) {
     const unsigned char *X = stg(st);
     nxt.advance(p);
-    if (tid == 0 && t + 1 < t_end) {  // prefetch the next tile into the other stage
+    if (DIRECT) {
+      // (the stage is refilled by the last warp done with it: see below)
+    } else if (tid == 0 && t + 1 < t_end) {  // prefetch the next tile into the other stage
 #if MM_MED_SPLIT
       if (it > 0) mbar_wait(&bars[2 + (st ^ 1)], ((it - 1) >> 1) & 1);  // tile it-1 consumed it
 #endif
@@ -206,7 +234,7 @@ __global__ void __launch_bounds__(NT, 2)
     const int64_t row = cur.row, u0 = cur.u0;
     const int tout = cur.tout(p);
     const int64_t ab0 = u0 / B;  // far block index (within the row) of group 0
-    mbar_wait(&bars[st], (it >> 1) & 1);
+    mbar_wait(&bars[st], (it / NSTG) & 1);
     if (patch_tail<S>(p, stg(st), row, u0, tout + w - 1, tid)) __syncthreads();
 
     // ------------------------------------------------- far chunk: prefix
@@ -214,6 +242,7 @@ __global__ void __launch_bounds__(NT, 2)
     // folded with the local suffix of the near chunk (carries go into cx/cn)
     T ux[E], un[E];
     T cx, cn;
+    T dgx, dgn;  // DIRECT: the gap H_{g-1}
     {
       T ya[E], yb[E];
       Src::template load<E>(X, tid * E + w - 1, u0, ya, yb);
@@ -225,10 +254,12 @@ __global__ void __launch_bounds__(NT, 2)
         un[k] = Ord<T>::mn(un[k - 1], yb[k]);
       }
       T hx, hn, tx, tn;
-      h_part(ya, ux[E - 1], un[E - 1], __shfl_sync(0xffffffffu, ya[E - 1], glast), hx, tn);
-      if (TWO) h_part(yb, ux[E - 1], un[E - 1], __shfl_sync(0xffffffffu, yb[E - 1], glast), tx, hn);
-      else hn = tn;
-      grp_reduce<T, G>(hx, hn);
+      if (!DIRECT) {
+        h_part(ya, ux[E - 1], un[E - 1], __shfl_sync(0xffffffffu, ya[E - 1], glast), hx, tn);
+        if (TWO) h_part(yb, ux[E - 1], un[E - 1], __shfl_sync(0xffffffffu, yb[E - 1], glast), tx, hn);
+        else hn = tn;
+        grp_reduce<T, G>(hx, hn);
+      }
       T ax = ux[E - 1], an = un[E - 1];  // group-inclusive prefix of chunk maxima
       grp_scan_up<T, G>(ax, an, gl);
       cx = shfl_up(ax, 1);
@@ -237,7 +268,26 @@ __global__ void __launch_bounds__(NT, 2)
         cx = ya[0];
         cn = yb[0];
       }
-      if (gl == G - 1) {  // publish far block aggregates G_g, H_g
+      if (DIRECT) {
+        // gap = H_{g-1}: this lane's chunk of F_{g-1} (B before its far chunk)
+        hx = hn = cx;  // (placeholders: replaced below when r' > 0)
+        if (g.rp > 0) {
+          T za[E], zb[E];
+          Src::template load<E>(X, tid * E + w - 1 - B, u0, za, zb);
+          T zx = za[0], zn = zb[0];
+#pragma unroll
+          for (int k = 1; k < E; ++k) {
+            zx = Ord<T>::mx(zx, za[k]);
+            zn = Ord<T>::mn(zn, zb[k]);
+          }
+          h_part(za, zx, zn, __shfl_sync(0xffffffffu, za[E - 1], glast), hx, tn);
+          if (TWO) h_part(zb, zx, zn, __shfl_sync(0xffffffffu, zb[E - 1], glast), tx, hn);
+          else hn = tn;
+          grp_reduce<T, G>(hx, hn);
+        }
+        dgx = hx;
+        dgn = hn;
+      } else if (gl == G - 1) {  // publish far block aggregates G_g, H_g
         const int ri = (int)((ab0 + grp) & RMASK);
         Rgx[ri] = ax;
         Rgn[ri] = an;
@@ -282,9 +332,11 @@ __global__ void __launch_bounds__(NT, 2)
       }
     };
 #if MM_MED_SPLIT
-    far_blocks_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive1(&bars[4]);  // this warp's ring entries are written
+    if (!DIRECT) {
+      far_blocks_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(&bars[4]);  // this warp's ring entries are written
+    }
 #endif
 
     // ------------------------------------------------ near chunk: suffix
@@ -312,6 +364,19 @@ __global__ void __launch_bounds__(NT, 2)
       cn = Ord<T>::mn(cn, en);
     }
 
+    if (DIRECT) {
+      // the last warp done with stage st refills it with tile it+NSTG: nobody waits
+      __syncwarp();
+      if (lane == 0 && atom_add_shared_u32(&done[st], 1u) == NT / 32 - 1) {
+        done[st] = 0;  // (every warp has arrived for this use; the next use follows the refill)
+        if (t + NSTG < t_end) stage_tile2<S>(p, &maps, stg(st), pf.row, pf.u0, pf.tout(p) + w - 1, &bars[st]);
+      }
+      pf.advance(p);
+      if (g.rp > 0) {
+        cx = Ord<T>::mx(cx, dgx);
+        cn = Ord<T>::mn(cn, dgn);
+      }
+    } else {
 #if MM_MED_SPLIT
     __syncwarp();
     if (lane == 0) mbar_arrive1(&bars[2 + st]);  // this warp is done with the stage
@@ -321,7 +386,7 @@ __global__ void __launch_bounds__(NT, 2)
     __syncthreads();
 #endif
 
-    // ---------------------------------------------------------- gap + out
+    // ---------------------------------------------------------- gap
     if (g.qp > 0 || g.rp > 0) {
       const int64_t b0 = ab0 + grp - g.qp - 1;  // far block F_{g-q'-1}
       T mx, mn;
@@ -339,6 +404,8 @@ __global__ void __launch_bounds__(NT, 2)
       cx = Ord<T>::mx(cx, mx);
       cn = Ord<T>::mn(cn, mn);
     }
+    }  // !DIRECT
+    // ---------------------------------------------------------- out
     const int c0 = tid * E;
     {
       T ox[E], on[E];
@@ -354,7 +421,7 @@ __global__ void __launch_bounds__(NT, 2)
     // and the ring holds >= V + 2*NT/G entries, so the next tile's writes never
     // alias this tile's reads.  A fresh next tile rewrites the V entries before
     // it: wait for this tile's readers first.
-    if (t + 1 < t_end && g.V > 0 && (t + 1 - t_begin < g.need || nxt.u0 / TILE < g.need))
+    if (!DIRECT && t + 1 < t_end && g.V > 0 && (t + 1 - t_begin < g.need || nxt.u0 / TILE < g.need))
       __syncthreads();
     cur = nxt;
   }

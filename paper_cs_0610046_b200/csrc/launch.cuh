@@ -274,6 +274,10 @@ int medium_G(int64_t w) {
   return G;
 }
 
+#ifndef MM_MED_DIRECT  // 1: k1d_medium's ring-free variant whenever q' = 0 (see k1d_medium.cuh)
+#define MM_MED_DIRECT 1
+#endif
+
 // Block geometry of k1d_medium: B = E*G; D = w-1-B = q'B + r'.
 template <typename T>
 MedGeom medium_geom(int64_t w, int G) {
@@ -300,9 +304,28 @@ static int launch_medium_g(const Rows &p, const CUtensorMap &small, cudaStream_t
                              p.in_ld * (int64_t)sizeof(T), kBigRows);
     if (rc) return rc;
   }
+  const MedGeom g = medium_geom<T>(p.w, G);
+  // w-1 < 2B with a gap of >= 16 elements: groups reduce their own gap (no
+  // ring, no per-tile CTA barrier).  Measured on C2 (k1d_medium):
+  // w=1024 0.567 -> 0.531 ms, w=300 0.564 -> 0.535 ms; slower for G < 4, r' < 16
+  // (w=130) and r' = 0 (w = 2^k+1, where the barrier-synchronised write
+  // stream of the ring variant runs at 0.98-0.99 of the copy peak).
+  if constexpr (G >= 4) {
+    if (MM_MED_DIRECT && g.qp == 0 && g.rp >= 16) {
+      auto kern = k1d_medium<T, G, Epi, SameSrc<T>, true>;
+      static size_t attr = 0;
+      const size_t smem = MedLayout<T>::bytes(p.w, g.ring, MedStages<true>::N);
+      int rc = set_smem(kern, smem, attr);
+      if (rc) return rc;
+      int grid = 0;
+      rc = occupancy_grid(kern, smem, p.ntiles, grid);
+      if (rc) return rc;
+      kern<<<grid, NT, smem, s>>>(p, g, map, epi);
+      return note_cuda(cudaGetLastError());
+    }
+  }
   auto kern = k1d_medium<T, G, Epi>;
   static size_t attr = 0;
-  const MedGeom g = medium_geom<T>(p.w, G);
   const size_t smem = MedLayout<T>::bytes(p.w, g.ring);
   int rc = set_smem(kern, smem, attr);
   if (rc) return rc;

@@ -809,3 +809,25 @@ def test_batched_many_tiny_problems(cuda_device, n):
         win = np.lib.stride_tricks.sliding_window_view(a, w, axis=1)
         assert np.array_equal(mx.cpu().numpy(), win.max(axis=2)), (n, w)
         assert np.array_equal(mn.cpu().numpy(), win.min(axis=2)), (n, w)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.uint8, np.int16, np.int32],
+                         ids=lambda d: np.dtype(d).name)
+@pytest.mark.parametrize("w", [100, 300, 600, 1000, 1024])
+def test_medium_direct_gap(cuda_device, dtype, w):
+    """k1d_medium's ring-free variant (q' = 0, r' >= 16: each lane group reduces
+    its own gap, stages refilled by the last warp done with them): rows of 1-3
+    tiles with ragged tails (the shared-memory tail patch), CTA ranges of one or
+    two tiles, and repeated launches (the election counters and full barriers
+    carry over from tile to tile)."""
+    per16 = 16 // np.dtype(dtype).itemsize  # row pitches are whole 16-B vectors (header layout rule)
+    for rows, n in ((3, w + 5), (40, 4096 + w - 1), (29, 9000 + w + 13), (5, 3 * 4096 + w + 31)):
+        ld = -(-n // per16) * per16
+        a = synth.random_values(dtype, rows * ld, seed=w * 7 + rows).reshape(rows, ld)
+        x = torch.from_numpy(a).to(dev())
+        ex, en = oracle.batched(a, w, n=n)
+        for _ in range(3):
+            mx, mn = mm.maxmin_filter_batched(x, w, n=n)
+            torch.cuda.synchronize()
+            assert_same(mx, ex, f"max w={w} rows={rows} n={n}")
+            assert_same(mn, en, f"min w={w} rows={rows} n={n}")
