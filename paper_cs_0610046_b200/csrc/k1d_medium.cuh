@@ -127,12 +127,15 @@ struct MedLayoutS {
 // the stage instead of reading the aggregate its predecessor published: no
 // ring, no cross-warp dependency and no per-tile CTA barrier.  Three stages;
 // a stage is recycled once every warp has arrived on its "empty" mbarrier.
+// NS (ring variant): 2 stages, the next tile prefetched at the start of a
+// tile; or 3, the tile it+3 issued right after tile it's barrier.
 template <int DIRECT>
 struct MedStages {
   static constexpr int N = DIRECT ? 3 : 2;
 };
 
-template <typename T, int G, class Epi = StoreEpi, class Src = SameSrc<T>, bool DIRECT = false>
+template <typename T, int G, class Epi = StoreEpi, class Src = SameSrc<T>, bool DIRECT = false,
+          int NS = MedStages<DIRECT>::N>
 __global__ void __launch_bounds__(NT, 2)
     k1d_medium(Rows p, MedGeom g, const __grid_constant__ TmaMaps maps, Epi epi = Epi()) {
   using Lay = MedLayout<T>;
@@ -150,7 +153,9 @@ __global__ void __launch_bounds__(NT, 2)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *base = smem_align1024(smem_raw);
   auto stg = [&](int i) { return base + i * SB; };
-  constexpr int NSTG = MedStages<DIRECT>::N;
+  constexpr int NSTG = NS;
+  static_assert(!DIRECT || NS == 3, "the ring-free variant runs three stages");
+  static_assert(!MM_MED_SPLIT || NS == 2, "the split-barrier build runs two stages");
   T *Rgx = reinterpret_cast<T *>(base + NSTG * SB);  // ring of far-block aggregates (unused if DIRECT)
   T *Rgn = Rgx + g.ring;
   T *Rhx = Rgn + g.ring;
@@ -177,8 +182,8 @@ __global__ void __launch_bounds__(NT, 2)
     prefetch_tmap(&maps.small);
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
+    if (NSTG == 3) mbar_init(&bars[2], 1);  // stage 2 full
     if (DIRECT) {
-      mbar_init(&bars[2], 1);  // stage 2 full
       for (int i = 0; i < NSTG; ++i) reinterpret_cast<uint32_t *>(bars + NSTG)[i] = 0;  // stage i: warps done
     }
 #if MM_MED_SPLIT
@@ -193,12 +198,12 @@ __global__ void __launch_bounds__(NT, 2)
   uint32_t *done = reinterpret_cast<uint32_t *>(bars + NSTG);  // DIRECT: per stage, warps done with it
   if (tid == 0 && t_begin < t_end) {
     stage_tile2<S>(p, &maps, stg(0), cur.row, cur.u0, cur.tout(p) + w - 1, &bars[0]);
-    for (int k = 1; DIRECT && k < NSTG; ++k) {
+    for (int k = 1; NSTG == 3 && k < NSTG; ++k) {
       pf.advance(p);
       if (t_begin + k < t_end) stage_tile2<S>(p, &maps, stg(k), pf.row, pf.u0, pf.tout(p) + w - 1, &bars[k]);
     }
   }
-  if (DIRECT) {
+  if (NSTG == 3) {
     pf = cur;
     for (int k = 0; k < NSTG; ++k) pf.advance(p);
   }
@@ -223,8 +228,8 @@ __global__ void __launch_bounds__(NT, 2)
   for (int64_t t = t_begin; t < t_end; ++t, ++it, st = st + 1 == NSTG ? 0 : st + 1) {
     const unsigned char *X = stg(st);
     nxt.advance(p);
-    if (DIRECT) {
-      // (the stage is refilled by the last warp done with it: see below)
+    if (NSTG == 3) {
+      // (the stage is refilled once every warp is done with it: see below)
     } else if (tid == 0 && t + 1 < t_end) {  // prefetch the next tile into the other stage
 #if MM_MED_SPLIT
       if (it > 0) mbar_wait(&bars[2 + (st ^ 1)], ((it - 1) >> 1) & 1);  // tile it-1 consumed it
@@ -384,6 +389,10 @@ __global__ void __launch_bounds__(NT, 2)
 #else
     far_blocks_before();
     __syncthreads();
+    if (NSTG == 3) {  // every warp is done with stage st: refill it with tile it+3
+      if (tid == 0 && t + NSTG < t_end) stage_tile2<S>(p, &maps, stg(st), pf.row, pf.u0, pf.tout(p) + w - 1, &bars[st]);
+      pf.advance(p);
+    }
 #endif
 
     // ---------------------------------------------------------- gap

@@ -274,6 +274,9 @@ int medium_G(int64_t w) {
   return G;
 }
 
+#ifndef MM_MED_RING3  // 1: k1d_medium's ring variant with three stages where two CTAs per SM fit
+#define MM_MED_RING3 1
+#endif
 #ifndef MM_MED_DIRECT  // 1: k1d_medium's ring-free variant whenever q' = 0 (see k1d_medium.cuh)
 #define MM_MED_DIRECT 1
 #endif
@@ -305,13 +308,18 @@ static int launch_medium_g(const Rows &p, const CUtensorMap &small, cudaStream_t
     if (rc) return rc;
   }
   const MedGeom g = medium_geom<T>(p.w, G);
-  // w-1 < 2B with a gap of >= 16 elements: groups reduce their own gap (no
-  // ring, no per-tile CTA barrier).  Measured on C2 (k1d_medium):
-  // w=1024 0.567 -> 0.531 ms, w=300 0.564 -> 0.535 ms; slower for G < 4, r' < 16
-  // (w=130) and r' = 0 (w = 2^k+1, where the barrier-synchronised write
-  // stream of the ring variant runs at 0.98-0.99 of the copy peak).
-  if constexpr (G >= 4) {
-    if (MM_MED_DIRECT && g.qp == 0 && g.rp >= 16) {
+  // Variant and stage count by measurement on C2 (k1d_medium;
+  // profiles/round2/session3/ab_medium_*.txt):
+  //  * ring-free (DIRECT: groups reduce their own gap, no per-tile CTA
+  //    barrier) for q' = 0, G >= 16 and a gap of at least half a block:
+  //    w=1024 0.567 -> 0.531 ms (three-stage ring: 0.549);
+  //  * the ring variant with three stages where it carries a gap (q' > 0, or
+  //    r' > 0 with G >= 8): w=130 0.539 -> 0.522, w=600 0.572 -> 0.537,
+  //    w=1025 0.547 -> 0.519, C5 w=4096 2.359 -> 2.295 ms;
+  //  * two stages otherwise: gap-free (r' = 0) and G <= 4 windows run at
+  //    0.94-0.99 of the copy peak with two and ~0.88 with three.
+  if constexpr (G >= 16) {
+    if (MM_MED_DIRECT && g.qp == 0 && 2 * g.rp >= g.B) {
       auto kern = k1d_medium<T, G, Epi, SameSrc<T>, true>;
       static size_t attr = 0;
       const size_t smem = MedLayout<T>::bytes(p.w, g.ring, MedStages<true>::N);
@@ -323,6 +331,19 @@ static int launch_medium_g(const Rows &p, const CUtensorMap &small, cudaStream_t
       kern<<<grid, NT, smem, s>>>(p, g, map, epi);
       return note_cuda(cudaGetLastError());
     }
+  }
+  if (MM_MED_RING3 && (g.qp > 0 || (g.rp > 0 && G >= 8)) &&
+      2 * (MedLayout<T>::bytes(p.w, g.ring, 3) + 1024) <= 228 * 1024) {
+    auto kern = k1d_medium<T, G, Epi, SameSrc<T>, false, 3>;
+    static size_t attr = 0;
+    const size_t smem = MedLayout<T>::bytes(p.w, g.ring, 3);
+    int rc = set_smem(kern, smem, attr);
+    if (rc) return rc;
+    int grid = 0;
+    rc = occupancy_grid(kern, smem, p.ntiles, grid);
+    if (rc) return rc;
+    kern<<<grid, NT, smem, s>>>(p, g, map, epi);
+    return note_cuda(cudaGetLastError());
   }
   auto kern = k1d_medium<T, G, Epi>;
   static size_t attr = 0;
