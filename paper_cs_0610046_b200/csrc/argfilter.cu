@@ -444,9 +444,23 @@ struct ArgEpi {
 
 template <typename S, int G>
 int launch_arg_medium_g(const Rows &p, const TmaMaps &maps, const ArgEpi<S> &epi, cudaStream_t s) {
+  const MedGeom g = medium_geom<uint64_t>(p.w, G);
+  // three stages where the tile carries a gap (launch.cuh, launch_medium_g)
+  if (MM_MED_RING3 && (g.qp > 0 || (g.rp > 0 && G >= 8)) &&
+      2 * (MedLayoutS<uint64_t, S>::bytes(p.w, g.ring, 3) + 1024) <= 228 * 1024) {
+    auto kern = k1d_medium<uint64_t, G, ArgEpi<S>, ArgSrc<S>, false, 3>;
+    static size_t attr = 0;
+    const size_t smem = MedLayoutS<uint64_t, S>::bytes(p.w, g.ring, 3);
+    int rc = set_smem(kern, smem, attr);
+    if (rc) return rc;
+    int grid = 0;
+    rc = occupancy_grid(kern, smem, p.ntiles, grid);
+    if (rc) return rc;
+    kern<<<grid, NT, smem, s>>>(p, g, maps, epi);
+    return note_cuda(cudaGetLastError());
+  }
   auto kern = k1d_medium<uint64_t, G, ArgEpi<S>, ArgSrc<S>>;
   static size_t attr = 0;
-  const MedGeom g = medium_geom<uint64_t>(p.w, G);
   const size_t smem = MedLayoutS<uint64_t, S>::bytes(p.w, g.ring);
   int rc = set_smem(kern, smem, attr);
   if (rc) return rc;
