@@ -72,7 +72,7 @@ __device__ __forceinline__ T warp_min(T v) {
 #define MM_LW_STATS 0
 #endif
 
-template <typename T>
+template <typename T, bool L3 = false>
 struct LwGeo {
   using W = WarpGeo<T>;
   static constexpr int E = W::E, WT = W::WT, RW = W::RW, VEC = W::VEC;
@@ -80,9 +80,15 @@ struct LwGeo {
   // far chunk = NROWS swizzled rows (a 1024-B aligned buffer like a near
   // chunk) + the one row past them, staged unswizzled into a shared block of
   // 128-B rows (so four far stages cost what three 17-row buffers would)
-  static constexpr int NFAR = 4, NNEAR = 2;  // far chunks three jobs ahead, near one
-  static constexpr int NTAB = 8;             // group-table stages (a warp leads its CTA by <= 2 jobs)
-  static constexpr int NTK = 8;              // ticket ring {tk, row, gi}: published four jobs ahead
+  // L3 = false: far chunks three jobs ahead (published two ahead), two near
+  // stages (one job ahead); ticket ring of 8, tickets put four jobs ahead.
+  // L3 = true: far chunks four jobs ahead (published three ahead) in the same
+  // shared memory: one near stage, reloaded for job i+1 as soon as job i has
+  // consumed it; ticket ring of 16, tickets put five jobs ahead.  Group-table
+  // stages: 8 (a warp leads its CTA by <= 2 or 3 jobs).
+  static constexpr int NFAR = L3 ? 5 : 4, NNEAR = L3 ? 1 : 2;
+  static constexpr int NTAB = 8;
+  static constexpr int NTK = L3 ? 16 : 8;
   static constexpr int WARP_SMEM = (NFAR + NNEAR) * NEAR;
   static constexpr int XROWS = NWARP * NFAR * 128;  // the extra far rows of every warp and stage
   // tail: per warp NFAR+NNEAR mbarriers; per table stage one mbarrier, one
@@ -136,6 +142,9 @@ __device__ __forceinline__ uint64_t lw_wait(const uint64_t *s, LwStats &st) {
 #endif
 }
 
+#ifndef MM_LW_L3_QMAX  // publication lead of three jobs for q <= this (the launch picks L3)
+#define MM_LW_L3_QMAX 255
+#endif
 #ifndef MM_LW_NW0  // gap words per lane loaded before the scans (nent <= 32*NW0; 4: q <= 504)
 #define MM_LW_NW0 4
 #endif
@@ -143,9 +152,9 @@ __device__ __forceinline__ uint64_t lw_wait(const uint64_t *s, LwStats &st) {
 #define MM_LW_MINB 2
 #endif
 
-template <typename T, int SH>
+template <typename T, int SH, bool L3>
 __global__ void __launch_bounds__(NT, MM_LW_MINB) k1d_lw(Rows p, LwArgs g, void *ws, const __grid_constant__ TmaMaps maps) {
-  using Geo = LwGeo<T>;
+  using Geo = LwGeo<T, L3>;
   constexpr int E = Geo::E, WT = Geo::WT, RW = Geo::RW;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *base = smem_align1024(smem_raw);
@@ -280,7 +289,7 @@ __global__ void __launch_bounds__(NT, MM_LW_MINB) k1d_lw(Rows p, LwArgs g, void 
     mbar_arrive1(tkbar(s));
   };
   auto wait_ticket = [&](int64_t job) {  // every lane, once per job (slot reused 8 jobs later)
-    mbar_wait(tkbar((int)(job & (Geo::NTK - 1))), (uint32_t)((job >> 3) & 1));
+    mbar_wait(tkbar((int)(job & (Geo::NTK - 1))), (uint32_t)((job / Geo::NTK) & 1));
   };
   auto pos = [&](int64_t job) {  // (after wait_ticket(job))
     const int4 t = *tkval((int)(job & (Geo::NTK - 1)));
@@ -391,8 +400,13 @@ __global__ void __launch_bounds__(NT, MM_LW_MINB) k1d_lw(Rows p, LwArgs g, void 
   };
 
   // ------------------------------------------------------------ process
-  auto process = [&](const Pos &j, int fs, int ns, int ts) {
-    if (!j.near) return;
+  // next_near (LEAD3): after this job's near chunk is in registers, lane 0
+  // stages the next job's into the single near stage
+  auto process = [&](const Pos &j, int fs, int ns, int ts, const Pos *next_near) {
+    if (!j.near) {
+      if (next_near && lane == 0) load_near(*next_near, 0);
+      return;
+    }
     const int64_t row = j.row;
     const int64_t u0 = (int64_t)j.x * WT;
     // gap words first: their latency overlaps the scans
@@ -446,6 +460,15 @@ __global__ void __launch_bounds__(NT, MM_LW_MINB) k1d_lw(Rows p, LwArgs g, void 
       }
       T ex = shfl_down(bx, 1), en = shfl_down(bn, 1);
       if (lane == 31) ex = en = seed;
+      if (next_near) {
+        // every lane's near values are consumed (the scan above used them):
+        // the single near stage takes the next job's chunk
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          load_near(*next_near, 0);
+        }
+      }
       Cx = Ord<T>::mx(Cx, ex);
       Cn = Ord<T>::mn(Cn, en);
     }
@@ -518,6 +541,58 @@ __global__ void __launch_bounds__(NT, MM_LW_MINB) k1d_lw(Rows p, LwArgs g, void 
   };
 
   // ------------------------------------------------------------ pipeline
+if constexpr (L3) {
+  // job i: far stage i%5 (loaded four jobs ahead, published three ahead),
+  // the near stage, table stage i%8, ticket slot i%16 (put five jobs ahead)
+  const bool ticketer = warp == 0 && lane == 0;
+  unsigned int pend = 0;  // warp 0 lane 0: the ticket of job i+6, in flight during job i
+  if (ticketer) {
+    unsigned t[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) t[i] = atomicAdd(counter, 1u);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) put_ticket(i, (int)t[i]);
+    pend = atomicAdd(counter, 1u);
+  }
+  for (int i = 0; i < 5; ++i) wait_ticket(i);
+  if (lane == 0) {
+    for (int i = 0; i < 4; ++i) load_far(pos(i), i);
+    load_near(pos(0), 0);
+  }
+  uint32_t fph = 0, nph = 0, tph = 0;  // barrier parities per stage (bit s)
+  auto wait_far = [&](int s) {
+    mbar_wait(&fbar[s], (fph >> s) & 1u);
+    fph ^= 1u << s;
+  };
+  for (int i = 0; i < 3; ++i) {
+    wait_far(i);
+    publish(pos(i), i, i);
+  }
+  int64_t job = 0;
+  int fs = 0;  // job % 5
+  while (pos(job).live) {
+    const int ts = (int)(job & 7);
+    const int fl = fs == 0 ? 4 : fs - 1;  // (job+4) % 5: job-1's stage, now free
+    const int fp = fl == 0 ? 4 : fl - 1;  // (job+3) % 5
+    if (ticketer) {
+      put_ticket(job + 5, (int)pend);
+      pend = atomicAdd(counter, 1u);
+    }
+    if (lane == 0) load_far(pos(job + 4), fl);
+    wait_far(fp);
+    publish(pos(job + 3), fp, (int)((job + 3) & 7));  // job i+3 goes public before job i waits on anything
+    mbar_wait(&nbar[0], nph);
+    nph ^= 1u;
+    const Pos j0 = pos(job), j1 = pos(job + 1);
+    if (j0.near) mbar_wait(tbar(ts), (tph >> ts) & 1u);
+    tph ^= 1u << ts;
+    process(j0, fs, 0, ts, &j1);
+    __syncwarp();  // stage fs is reloaded only after every lane read it
+    ++job;
+    fs = fs == 4 ? 0 : fs + 1;
+    wait_ticket(job + 4);
+  }
+} else {
   // job i: far stage i%4, near stage i%2, table stage i%8, ticket slot i%8
   const bool ticketer = warp == 0 && lane == 0;
   unsigned int pend = 0;  // warp 0 lane 0: the ticket of job i+5, in flight during job i
@@ -567,11 +642,12 @@ __global__ void __launch_bounds__(NT, MM_LW_MINB) k1d_lw(Rows p, LwArgs g, void 
     // the table stage of job i is complete once all 8 warps published it
     if (j0.near) mbar_wait(tbar(ts), (tph >> ts) & 1u);
     tph ^= 1u << ts;
-    process(j0, fs, ns, ts);
+    process(j0, fs, ns, ts, nullptr);
     __syncwarp();  // stages fs and ns are reloaded only after every lane read them
     ++job;
     wait_ticket(job + 3);
   }
+}  // L3
 #if MM_LW_STATS
   {
     unsigned long long *st = reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + 64);

@@ -430,17 +430,21 @@ static int launch_lw(const Rows &p, void *ws, size_t ws_bytes, cudaStream_t s) {
     // every word's flag: one memset (256 B per 4096 outputs)
     cudaError_t e = cudaMemsetAsync(ws, 0, LwWs<T>::bytes(g), s);
     if (e != cudaSuccess) return note_cuda(e);
-    // the far chunk's in-vector shift is a template parameter for 4-byte types
-    auto kern = k1d_lw<T, -1>;
+    // the far chunk's in-vector shift is a template parameter for 4-byte
+    // types; the publication lead is three jobs for q <= MM_LW_L3_QMAX (C2
+    // w=65536, q=127: 0.720 -> 0.690 ms) and two otherwise (C5 w=262144,
+    // q=511: 3.215 ms with two, 3.276 with three)
+    const bool l3 = g.q <= MM_LW_L3_QMAX;
+    auto kern = l3 ? k1d_lw<T, -1, true> : k1d_lw<T, -1, false>;
     if constexpr (sizeof(T) == 4) {
       switch ((int)((p.w - 1) % Geo::VEC)) {
-        case 0: kern = k1d_lw<T, 0>; break;
-        case 1: kern = k1d_lw<T, 1>; break;
-        case 2: kern = k1d_lw<T, 2>; break;
-        default: kern = k1d_lw<T, 3>; break;
+        case 0: kern = l3 ? k1d_lw<T, 0, true> : k1d_lw<T, 0, false>; break;
+        case 1: kern = l3 ? k1d_lw<T, 1, true> : k1d_lw<T, 1, false>; break;
+        case 2: kern = l3 ? k1d_lw<T, 2, true> : k1d_lw<T, 2, false>; break;
+        default: kern = l3 ? k1d_lw<T, 3, true> : k1d_lw<T, 3, false>; break;
       }
     }
-    constexpr size_t smem = Geo::BYTES;
+    const size_t smem = l3 ? LwGeo<T, true>::BYTES : LwGeo<T, false>::BYTES;
     rc = raise_smem_limit(reinterpret_cast<const void *>(kern), smem);
     if (rc) return rc;
     int grid = 0;
