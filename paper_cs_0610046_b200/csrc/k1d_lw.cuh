@@ -34,6 +34,12 @@
 // taken earlier by CTAs that are running (a CTA takes tickets only while it
 // runs) and that only wait on even lower groups -- no deadlock, no residency
 // assumption.
+//
+// Lead (template parameter L3, picked by the launch for q <= MM_LW_L3_QMAX):
+// the variant above publishes two jobs ahead; with L3 a warp stages far chunks
+// four jobs ahead and publishes job i+3, the fifth far stage taking the shared
+// memory of the second near stage -- the single near stage is reloaded for
+// job i+1 once job i's suffix scan has consumed it (k1d_lw).
 #pragma once
 
 #include "k1d_warp.cuh"
