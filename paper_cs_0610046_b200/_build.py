@@ -54,8 +54,12 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None,
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     objs = []
 
+    hdr_t = max(os.path.getmtime(h) for h in _deps() if not h.endswith(".cu"))
+
     def compile_one(src: str) -> str:
         obj = os.path.join(build_dir, os.path.basename(src)[:-3] + ".o")
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(hdr_t, os.path.getmtime(src)):
+            return obj  # newer than its source and every header
         cmd = [nvcc, *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

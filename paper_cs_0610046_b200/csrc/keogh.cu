@@ -22,9 +22,21 @@ struct KeoghEpi {
   const float *q;  // query, n samples
   int64_t r;
   double *acc;     // per row: the running sum of squares (the output, pre-sqrt)
+  // the excess of q_i over the envelope: the operand pair is selected in float
+  // ((q_i, U_i), (L_i, q_i) or (0, 0)), so each element costs one conversion
+  // pair and one subtraction in double -- the same value as the branch-wise form
+  __device__ __forceinline__ static double diff(float qv, float u, float l) {
+    const bool hi = qv > u, lo = qv < l;
+    const float a = hi ? qv : (lo ? l : 0.f), b = hi ? u : (lo ? qv : 0.f);
+    return (double)a - (double)b;
+  }
   __device__ __forceinline__ static double term(float qv, float u, float l) {
-    const double d = qv > u ? (double)qv - (double)u : (qv < l ? (double)l - (double)qv : 0.0);
+    const double d = diff(qv, u, l);
     return d * d;
+  }
+  __device__ __forceinline__ static double acc_term(double s, float qv, float u, float l) {
+    const double d = diff(qv, u, l);
+    return fma(d, d, s);  // one DFMA per element
   }
   template <typename T, int E>
   __device__ __forceinline__ void operator()(const Rows &p, int64_t row, int64_t j0, int cnt, const T (&ox)[E],
@@ -36,13 +48,15 @@ struct KeoghEpi {
 #pragma unroll
       for (int k = 0; k < E; k += 4) {
         const float4 v = __ldg(reinterpret_cast<const float4 *>(qp + k));
-        s += term(v.x, ox[k], on[k]) + term(v.y, ox[k + 1], on[k + 1]) + term(v.z, ox[k + 2], on[k + 2]) +
-             term(v.w, ox[k + 3], on[k + 3]);
+        s = acc_term(s, v.x, ox[k], on[k]);
+        s = acc_term(s, v.y, ox[k + 1], on[k + 1]);
+        s = acc_term(s, v.z, ox[k + 2], on[k + 2]);
+        s = acc_term(s, v.w, ox[k + 3], on[k + 3]);
       }
     } else {
 #pragma unroll
       for (int k = 0; k < E; ++k)
-        if (k < cnt) s += term(__ldg(qp + k), ox[k], on[k]);
+        if (k < cnt) s = acc_term(s, __ldg(qp + k), ox[k], on[k]);
     }
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
