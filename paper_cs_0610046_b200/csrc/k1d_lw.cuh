@@ -30,7 +30,11 @@
 // i: its gap is the same-group prefix from the table (an mbarrier: every
 // warp's publish of job i happened two iterations earlier) plus <= 2 + 2q/8
 // global words of earlier groups, loaded before the scans and polled only if
-// not yet published.  A CTA only waits on lower groups; their tickets were
+// not yet published.  Every live job waits for its table stage, publish-only
+// jobs (tiles before a row's first window) too: that wait is what bounds a
+// warp's lead over its siblings to the publication lead, and the table, ticket
+// and far rings are sized for that bound (warp 0, the ticketer, has no other
+// wait on publish-only jobs).  A CTA only waits on lower groups; their tickets were
 // taken earlier by CTAs that are running (a CTA takes tickets only while it
 // runs) and that only wait on even lower groups -- no deadlock, no residency
 // assumption.
@@ -78,6 +82,22 @@ __device__ __forceinline__ T warp_min(T v) {
 #define MM_LW_STATS 0
 #endif
 
+#ifndef MM_LW_L3_QMAX  // publication lead of three jobs for q <= this (the launch picks L3)
+#define MM_LW_L3_QMAX 255
+#endif
+#ifndef MM_LW_TL3  // L3: tickets put this many jobs ahead (>= 5; slot reuse needs < NTK - 4)
+#define MM_LW_TL3 5
+#endif
+#ifndef MM_LW_TL2  // two-job lead: tickets put this many jobs ahead (>= 4; > 4 takes a 16-slot ring)
+#define MM_LW_TL2 4
+#endif
+#ifndef MM_LW_NW0  // gap words per lane loaded before the scans (nent <= 32*NW0; 4: q <= 504)
+#define MM_LW_NW0 4
+#endif
+#ifndef MM_LW_MINB  // resident CTAs per SM the register budget is sized for
+#define MM_LW_MINB 2
+#endif
+
 template <typename T, bool L3 = false>
 struct LwGeo {
   using W = WarpGeo<T>;
@@ -94,7 +114,7 @@ struct LwGeo {
   // stages: 8 (a warp leads its CTA by <= 2 or 3 jobs).
   static constexpr int NFAR = L3 ? 5 : 4, NNEAR = L3 ? 1 : 2;
   static constexpr int NTAB = 8;
-  static constexpr int NTK = L3 ? 16 : 8;
+  static constexpr int NTK = (L3 || MM_LW_TL2 > 4) ? 16 : 8;
   static constexpr int WARP_SMEM = (NFAR + NNEAR) * NEAR;
   static constexpr int XROWS = NWARP * NFAR * 128;  // the extra far rows of every warp and stage
   // tail: per warp NFAR+NNEAR mbarriers; per table stage one mbarrier, one
@@ -147,16 +167,6 @@ __device__ __forceinline__ uint64_t lw_wait(const uint64_t *s, LwStats &st) {
   return wait_slot(s);
 #endif
 }
-
-#ifndef MM_LW_L3_QMAX  // publication lead of three jobs for q <= this (the launch picks L3)
-#define MM_LW_L3_QMAX 255
-#endif
-#ifndef MM_LW_NW0  // gap words per lane loaded before the scans (nent <= 32*NW0; 4: q <= 504)
-#define MM_LW_NW0 4
-#endif
-#ifndef MM_LW_MINB  // resident CTAs per SM the register budget is sized for
-#define MM_LW_MINB 2
-#endif
 
 template <typename T, int SH, bool L3>
 __global__ void __launch_bounds__(NT, MM_LW_MINB) k1d_lw(Rows p, LwArgs g, void *ws, const __grid_constant__ TmaMaps maps) {
@@ -551,13 +561,15 @@ if constexpr (L3) {
   // job i: far stage i%5 (loaded four jobs ahead, published three ahead),
   // the near stage, table stage i%8, ticket slot i%16 (put five jobs ahead)
   const bool ticketer = warp == 0 && lane == 0;
-  unsigned int pend = 0;  // warp 0 lane 0: the ticket of job i+6, in flight during job i
+  constexpr int TL = MM_LW_TL3;
+  static_assert(TL >= 5 && TL + 4 < Geo::NTK, "ticket lead");
+  unsigned int pend = 0;  // warp 0 lane 0: the ticket of job i+TL+1, in flight during job i
   if (ticketer) {
-    unsigned t[5];
+    unsigned t[TL];
 #pragma unroll
-    for (int i = 0; i < 5; ++i) t[i] = atomicAdd(counter, 1u);
+    for (int i = 0; i < TL; ++i) t[i] = atomicAdd(counter, 1u);
 #pragma unroll
-    for (int i = 0; i < 5; ++i) put_ticket(i, (int)t[i]);
+    for (int i = 0; i < TL; ++i) put_ticket(i, (int)t[i]);
     pend = atomicAdd(counter, 1u);
   }
   for (int i = 0; i < 5; ++i) wait_ticket(i);
@@ -581,7 +593,7 @@ if constexpr (L3) {
     const int fl = fs == 0 ? 4 : fs - 1;  // (job+4) % 5: job-1's stage, now free
     const int fp = fl == 0 ? 4 : fl - 1;  // (job+3) % 5
     if (ticketer) {
-      put_ticket(job + 5, (int)pend);
+      put_ticket(job + TL, (int)pend);
       pend = atomicAdd(counter, 1u);
     }
     if (lane == 0) load_far(pos(job + 4), fl);
@@ -590,7 +602,11 @@ if constexpr (L3) {
     mbar_wait(&nbar[0], nph);
     nph ^= 1u;
     const Pos j0 = pos(job), j1 = pos(job + 1);
-    if (j0.near) mbar_wait(tbar(ts), (tph >> ts) & 1u);
+    // every live job waits for its table stage, publish-only ones too: this
+    // bounds how far a warp (warp 0 included, which takes no ticket waits) can
+    // run ahead of its siblings, so the table, ticket and far rings are never
+    // refilled under a slower warp
+    mbar_wait(tbar(ts), (tph >> ts) & 1u);
     tph ^= 1u << ts;
     process(j0, fs, 0, ts, &j1);
     __syncwarp();  // stage fs is reloaded only after every lane read it
@@ -601,13 +617,15 @@ if constexpr (L3) {
 } else {
   // job i: far stage i%4, near stage i%2, table stage i%8, ticket slot i%8
   const bool ticketer = warp == 0 && lane == 0;
-  unsigned int pend = 0;  // warp 0 lane 0: the ticket of job i+5, in flight during job i
+  constexpr int TL = MM_LW_TL2;
+  static_assert(TL >= 4 && TL + 3 < Geo::NTK, "ticket lead");
+  unsigned int pend = 0;  // warp 0 lane 0: the ticket of job i+TL+1, in flight during job i
   if (ticketer) {
-    unsigned t[4];
+    unsigned t[TL];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) t[i] = atomicAdd(counter, 1u);
+    for (int i = 0; i < TL; ++i) t[i] = atomicAdd(counter, 1u);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) put_ticket(i, (int)t[i]);
+    for (int i = 0; i < TL; ++i) put_ticket(i, (int)t[i]);
     pend = atomicAdd(counter, 1u);
   }
   for (int i = 0; i < 4; ++i) wait_ticket(i);
@@ -634,7 +652,7 @@ if constexpr (L3) {
   while (pos(job).live) {
     const int fs = (int)(job & 3), ns = (int)(job & 1), ts = (int)(job & 7);
     if (ticketer) {
-      put_ticket(job + 4, (int)pend);
+      put_ticket(job + TL, (int)pend);
       pend = atomicAdd(counter, 1u);
     }
     if (lane == 0) {
@@ -645,8 +663,9 @@ if constexpr (L3) {
     publish(pos(job + 2), (fs + 2) & 3, (ts + 2) & 7);  // job i+2 goes public before job i waits on anything
     wait_near(ns);
     const Pos j0 = pos(job);
-    // the table stage of job i is complete once all 8 warps published it
-    if (j0.near) mbar_wait(tbar(ts), (tph >> ts) & 1u);
+    // the table stage of job i is complete once all 8 warps published it; every
+    // live job waits for it, publish-only ones too (bounds the warps' spread)
+    mbar_wait(tbar(ts), (tph >> ts) & 1u);
     tph ^= 1u << ts;
     process(j0, fs, ns, ts, nullptr);
     __syncwarp();  // stages fs and ns are reloaded only after every lane read them

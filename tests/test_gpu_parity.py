@@ -135,6 +135,25 @@ def test_large_window_repeated(cuda_device, dtype):
             assert_same(mn, en, f"min w={w}")
 
 
+@pytest.mark.parametrize("w", [8193 + 512, 9000, 9600, 9985])
+def test_large_window_publish_only_rows(cuda_device, w):
+    """Rows only a few tiles longer than the window (n=10000, q = 17..19): most of
+    every row's groups are publish-only for warp 0 (its tile lies before the row's
+    first window), so warp 0 takes no waits of its own there.  Every live job
+    waits for its table stage (k1d_lw.cuh pipeline), which bounds how far warp 0
+    can run ahead of siblings stuck on gap polls; without it a longer ticket
+    lead (-DMM_LW_TL3=9) faulted here.  Repeated launches, 300 rows."""
+    rows, n = 300, 10_000
+    a = synth.random_values(np.float32, rows * n, seed=777).reshape(rows, n)
+    x = torch.from_numpy(a).to(dev())
+    ex, en = oracle.batched(a, w)
+    for _ in range(8):
+        mx, mn = mm.maxmin_filter_batched(x, w)
+        torch.cuda.synchronize()
+        assert_same(mx, ex, f"max w={w}")
+        assert_same(mn, en, f"min w={w}")
+
+
 def test_c3_shape_sample(cuda_device):
     """C3 layout [65536][4096] f32, w=129; parity on a 2048-row slice (full size in bench)."""
     rows = 2048
