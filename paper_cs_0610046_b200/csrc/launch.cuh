@@ -280,9 +280,6 @@ int medium_G(int64_t w) {
 #ifndef MM_MED_DIRECT  // 1: k1d_medium's ring-free variant whenever q' = 0 (see k1d_medium.cuh)
 #define MM_MED_DIRECT 1
 #endif
-#ifndef MM_MED_DIRECT_EPI  // 1: fused epilogues (no stores) take the ring-free variant at any q' = 0 gap
-#define MM_MED_DIRECT_EPI 0
-#endif
 
 // Block geometry of k1d_medium: B = E*G; D = w-1-B = q'B + r'.
 template <typename T>
@@ -322,8 +319,7 @@ static int launch_medium_g(const Rows &p, const CUtensorMap &small, cudaStream_t
   //  * two stages otherwise: gap-free (r' = 0) and G <= 4 windows run at
   //    0.94-0.99 of the copy peak with two and ~0.88 with three.
   if constexpr (G >= 16) {
-    constexpr bool fused = !std::is_same<Epi, StoreEpi>::value;
-    if (MM_MED_DIRECT && g.qp == 0 && (2 * g.rp >= g.B || (MM_MED_DIRECT_EPI && fused))) {
+    if (MM_MED_DIRECT && g.qp == 0 && 2 * g.rp >= g.B) {
       auto kern = k1d_medium<T, G, Epi, SameSrc<T>, true>;
       static size_t attr = 0;
       const size_t smem = MedLayout<T>::bytes(p.w, g.ring, MedStages<true>::N);
